@@ -1,0 +1,174 @@
+/*
+ * odescan_b200.h — C ABI of the B200-native parallel-in-time Newton solver.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `odescan` (arXiv 2511.01465).  Every entry point below replaces one
+ * reference interface; the citation after each declaration is the
+ * reference file:line (relative to /root/reference/pkg/src/odescan/) whose
+ * behaviour it reproduces.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch tensors),
+ *    fp64, C-contiguous, caller-owned.  Scalars are passed by value; small
+ *    descriptor structs (problem / stepper / config) are HOST pointers and are
+ *    copied by value into kernel parameters, so they may be freed on return.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call only enqueues work on that stream and returns immediately;
+ *    no call synchronises the device.
+ *  - Return value: ODX_OK (0) or a negative ODX_E* code.  No exception ever
+ *    crosses the ABI; odx_last_error() returns a thread-local message.
+ *  - The library keeps no global mutable state other than cached device
+ *    properties, so calls on different streams/devices may run concurrently.
+ *  - There is no CPU fallback: every compute entry point runs CUDA kernels
+ *    built for sm_100a, or fails with ODX_ECUDA / ODX_EUNSUPPORTED.
+ */
+#ifndef ODESCAN_B200_H
+#define ODESCAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ODX_ABI_VERSION 1
+
+/* ---- return codes ------------------------------------------------------ */
+#define ODX_OK            0
+#define ODX_EINVAL       (-1)  /* bad argument (ValueError on the Python side) */
+#define ODX_EUNSUPPORTED (-2)  /* no device functor / unsupported dim or stepper */
+#define ODX_ECUDA        (-3)  /* CUDA runtime error */
+#define ODX_EWORKSPACE   (-4)  /* workspace too small */
+
+/* ---- per-trajectory solve status (int32 status[b]) --------------------- */
+#define ODX_ST_MAXITER    0  /* ran max_iters updates (the reference's normal exit) */
+#define ODX_ST_CONVERGED  1  /* residual_tol or step_tol rule fired               */
+#define ODX_ST_NONFINITE  2  /* ||h||_inf = +-inf at iteration status_index
+                                (newton_pint.py:381-383, NonFiniteError)          */
+#define ODX_ST_SINGULAR   3  /* pivot < 1e-300 in block status_index
+                                (newton_pint.py:378-380, SingularDiagonalBlockError) */
+
+/* ---- ODE problems (device functors) ------------------------------------ */
+/* Reference plug-in type: OdeProblem(f_into, jac_into) problems.py:36-65.
+ * numba dispatchers cannot run on the GPU, so a problem crosses the ABI as
+ * (problem_id, dim, params) selecting a compiled device functor.            */
+#define ODX_PROB_LOGISTIC     0  /* params: r, K              problems.py:88-114  */
+#define ODX_PROB_VDP          1  /* params: mu                problems.py:117-147 */
+#define ODX_PROB_CARTPOLE     2  /* params: g, l, m_c, m_p    problems.py:162-194 */
+#define ODX_PROB_CARTPOLE_SQ  3  /* centripetal variant       problems.py:197-226 */
+#define ODX_PROB_DAHLQUIST    4  /* params: lambda            problems.py:248-272 */
+#define ODX_PROB_ROBERTSON    5  /* params: k1, k2, k3        problems.py:275-318 */
+#define ODX_PROB_LORENZ63     6  /* params: sigma, rho, beta  (BASELINE cfg 1/3)  */
+#define ODX_PROB_ALLEN_CAHN   7  /* params: eps, dx; dim = grid points (cfg 4)    */
+#define ODX_PROB_EXP_GROWTH   8  /* dy/dt = exp(y)  tests/test_newton_pint.py:28-46 */
+#define ODX_PROB_SQUARE       9  /* dy/dt = y^2     tests/test_newton_pint.py:49-68 */
+#define ODX_PROB_LINEAR      10  /* dx/dt = A x; params: A row-major (dim<=8)      */
+#define ODX_NUM_PROBLEMS     11
+
+#define ODX_MAX_PARAMS 64
+
+typedef struct odx_problem {
+    int32_t problem_id;
+    int32_t dim;
+    int32_t n_params;
+    int32_t reserved;
+    double  params[ODX_MAX_PARAMS];
+} odx_problem;
+
+/* ---- step maps ---------------------------------------------------------- */
+/* Reference: StepperIncrement{kind, tableau | weights} steppers.py:80-99.    */
+#define ODX_STEP_EXPLICIT_RK        0  /* tableau a (s x s, strictly lower), b (s) */
+#define ODX_STEP_IMPLICIT_WEIGHTED  1  /* g = dt (w_prev f(prev) + w_next f(next)) */
+#define ODX_MAX_STAGES 4
+
+typedef struct odx_stepper {
+    int32_t kind;
+    int32_t stages;                              /* explicit only, 1..4 */
+    double  a[ODX_MAX_STAGES * ODX_MAX_STAGES];  /* row-major s x s    */
+    double  b[ODX_MAX_STAGES];
+    double  w_prev, w_next;                      /* implicit only      */
+} odx_stepper;
+
+/* ---- Newton controls ---------------------------------------------------- */
+/* Reference: NewtonConfig(max_iters, residual_tol, record_residuals)
+ * newton_pint.py:119-138, plus the BASELINE step rule (step_tol) and a
+ * non-aborting fixed-iteration mode used for timing.      */
+typedef struct odx_newton_cfg {
+    int32_t max_iters;        /* >= 1                                        */
+    int32_t abort_nonfinite;  /* 1: stop with NONFINITE like solve(); 0: keep going */
+    double  residual_tol;     /* 0 disables; stop when ||h||_inf <= tol      */
+    double  step_tol;         /* 0 disables; stop when max|dx| of the last update < tol */
+} odx_newton_cfg;
+
+/* ---- library info -------------------------------------------------------- */
+int         odx_abi_version(void);
+const char* odx_last_error(void);
+/* 1 if (problem, stepper) has a compiled device path, else 0. */
+int         odx_supported(const odx_problem* P, const odx_stepper* S);
+
+/* ---- the solver ------------------------------------------------------------
+ * Replaces odescan.solve()  newton_pint.py:326-406 (batched over B
+ * independent trajectories).  X holds the initial guess on entry
+ * and the final iterate on exit (the guess policy is built by the caller,
+ * newton_pint.py:352-355).  For every trajectory b:
+ *   hist[b*(max_iters+1)+it]        = ||h(xi^(it))||_inf   (NaN-ignoring, _kernels.py:84-95)
+ *   scaled_hist[b*(max_iters+1)+it] = max|ce| (implicit) or == hist (explicit)
+ *   iters[b]   = iterations_run, status[b] = ODX_ST_*, status_index[b] = the
+ *   iteration (NONFINITE) or block index (SINGULAR), -1 otherwise.
+ * hist / scaled_hist may be NULL.  Workspace: odx_solve_workspace_bytes().   */
+size_t odx_solve_workspace_bytes(const odx_problem* P, const odx_stepper* S,
+                                 int64_t B, int64_t N, const odx_newton_cfg* C);
+int odx_solve(const odx_problem* P, const odx_stepper* S,
+              const double* x0, double* X, int64_t B, int64_t N, double dt,
+              const odx_newton_cfg* C,
+              double* hist, double* scaled_hist,
+              int32_t* iters, int32_t* status, int64_t* status_index,
+              void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- piecewise ops mirroring the reference's compiled loops ---------------- */
+/* _kernels.build_explicit  _kernels.py:299-342 (+ _rk_increment_with_jac :261-296) */
+int odx_build_explicit(const odx_problem* P, const odx_stepper* S,
+                       const double* x0, const double* X, int64_t N, double dt,
+                       double* Fe, double* ce, double* h, void* stream);
+/* _kernels.build_implicit  _kernels.py:393-464; *first_bad (device int64) = -1 or k */
+int odx_build_implicit(const odx_problem* P, const odx_stepper* S,
+                       const double* x0, const double* X, int64_t N, double dt,
+                       double* Fe, double* ce, double* h, int64_t* first_bad,
+                       void* stream);
+/* _kernels.scan_affine  _kernels.py:116-233 (inclusive scan, Fp may be NULL) */
+size_t odx_scan_affine_workspace_bytes(int64_t N, int32_t d);
+int odx_scan_affine(const double* Fin, const double* cin, int64_t N, int32_t d,
+                    double* Fp, double* cp, void* workspace,
+                    size_t workspace_bytes, void* stream);
+/* _kernels.max_abs  _kernels.py:84-95 (NaN-ignoring); *out is a device double */
+int odx_max_abs(const double* A, int64_t n, int32_t d, double* out, void* stream);
+/* _kernels.add_inplace  _kernels.py:98-103 */
+int odx_add_inplace(double* X, const double* U, int64_t n, int32_t d, void* stream);
+
+/* ---- time-sharded solve (one rank per GPU) ----------------------
+ * Rank r owns steps [offset, offset+N_local) of one trajectory.  Per Newton
+ * iteration: odx_shard_local() builds the local elements from X_local and the
+ * halo state (the last state of rank r-1, or x0 on rank 0), scans them, and
+ * writes a summary record of ODX_SHARD_REC(d) doubles:
+ *   [F_agg (d*d) | c_agg (d) | x_last (d) | rn | sc | step_prev | bad]
+ * The caller all-gathers the records (NCCL), then odx_shard_fixup() prefixes
+ * the carries of ranks < r, applies the carry to the local prefixes and
+ * writes X_local += dx.  Reference path: the same solve() loop
+ * newton_pint.py:366-396 with the scan split across ranks.                    */
+#define ODX_SHARD_REC(d) ((d) * (d) + 2 * (d) + 4)
+size_t odx_shard_workspace_bytes(const odx_problem* P, const odx_stepper* S,
+                                 int64_t N_local);
+int odx_shard_local(const odx_problem* P, const odx_stepper* S,
+                    const double* halo, const double* X_local, int64_t N_local,
+                    int64_t offset, double dt, double* record,
+                    void* workspace, size_t workspace_bytes, void* stream);
+int odx_shard_fixup(const odx_problem* P, const double* records, int32_t rank,
+                    int32_t nranks, double* X_local, int64_t N_local,
+                    double* step_out, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ODESCAN_B200_H */
