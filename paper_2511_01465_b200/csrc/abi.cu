@@ -1,0 +1,310 @@
+// abi.cu — the extern "C" boundary (include/odescan_b200.h).  Validates
+// descriptors, converts them to kernel parameters and dispatches to the
+// templated device paths.  No exception crosses this boundary; errors are
+// negative codes plus a thread-local message (odx_last_error).
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "dispatch.cuh"
+#include "solve_small.cuh"
+
+namespace odx {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+int num_sms() {
+    static std::mutex mu;
+    static std::unordered_map<int, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev] = n;
+    return n;
+}
+
+bool fill_params(const odx_problem* P, ProbParams& pp) {
+    if (!P || P->n_params < 0 || P->n_params > ODX_MAX_PARAMS) return false;
+    std::memset(&pp, 0, sizeof(pp));
+    for (int i = 0; i < P->n_params; i++) pp.p[i] = P->params[i];
+    return true;
+}
+
+bool fill_coefs(const odx_stepper* S, double dt, StepCoefs& sc) {
+    if (!S) return false;
+    std::memset(&sc, 0, sizeof(sc));
+    sc.dt = dt;
+    if (S->kind == ODX_STEP_EXPLICIT_RK) {
+        const int s = S->stages;
+        if (s < 1 || s > ODX_MAX_STAGES) return false;
+        for (int i = 0; i < s; i++) {
+            for (int j = 0; j < s; j++) {
+                if (j >= i && S->a[i * s + j] != 0.0) return false;  // explicit only
+                sc.dta[i * s + j] = dt * S->a[i * s + j];
+            }
+            sc.b[i] = S->b[i];
+        }
+        sc.stages = s;
+        return true;
+    }
+    if (S->kind == ODX_STEP_IMPLICIT_WEIGHTED) {
+        sc.w_prev = S->w_prev;
+        sc.w_next = S->w_next;
+        sc.dt_wprev = dt * S->w_prev;
+        sc.dt_wnext = dt * S->w_next;
+        sc.stages = 1;
+        return true;
+    }
+    return false;
+}
+
+template <class P, int KIND, int S>
+int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
+                size_t* need);
+template <class P, int KIND, int S>
+int build_op(const ProbParams& pp, const StepCoefs& sc, const double* x0, const double* X,
+             long long N, double* Fe, double* ce, double* h, long long* first_bad,
+             cudaStream_t st);
+int scan_op(const double* F, const double* c, long long N, int d, double* Fp, double* cp,
+            void* ws, size_t ws_bytes, cudaStream_t st);
+size_t scan_op_ws(long long N, int d);
+int max_abs_op(const double* A, long long n, int d, double* out, cudaStream_t st);
+int add_op(double* X, const double* U, long long n, int d, cudaStream_t st);
+
+// d = 64 dense path (solve_dense.cu)
+int dense_supported(const odx_problem* P, const odx_stepper* S);
+int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
+                size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
+int dense_build_op(const odx_problem* P, const odx_stepper* S, const StepCoefs& sc,
+                   const double* x0, const double* X, long long N, double* Fe, double* ce,
+                   double* h, long long* first_bad, cudaStream_t st);
+int dense_scan_op(const double* F, const double* c, long long N, int d, double* Fp, double* cp,
+                  void* ws, size_t ws_bytes, cudaStream_t st);
+size_t dense_scan_op_ws(long long N, int d);
+
+// Stage-count / kind dispatch for a fixed problem type.
+template <class P, class Fn>
+int with_stepper(const odx_stepper* S, Fn&& fn) {
+    if (S->kind == ODX_STEP_IMPLICIT_WEIGHTED) return fn.template operator()<P, 1, 1>();
+    switch (S->stages) {
+    case 1: return fn.template operator()<P, 0, 1>();
+    case 2: return fn.template operator()<P, 0, 2>();
+    case 3: return fn.template operator()<P, 0, 3>();
+    case 4: return fn.template operator()<P, 0, 4>();
+    default: return ODX_EUNSUPPORTED;
+    }
+}
+
+struct ProbeFn {
+    const odx_stepper* S;
+    template <class PP>
+    int operator()() {
+        return with_stepper<PP>(S, [&]<class Q, int K, int SS>() { return 1; }) == 1 ? 1 : 0;
+    }
+};
+
+struct SolveFn {
+    const odx_stepper* S;
+    SolveParams* p;
+    void* ws;
+    size_t ws_bytes;
+    cudaStream_t st;
+    bool query;
+    size_t* need;
+    template <class PP>
+    int operator()() {
+        return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
+            return solve_small<Q, K, SS>(*p, ws, ws_bytes, st, query, need);
+        });
+    }
+};
+
+struct BuildFn {
+    const odx_stepper* S;
+    const ProbParams* pp;
+    const StepCoefs* sc;
+    const double *x0, *X;
+    long long N;
+    double *Fe, *ce, *h;
+    long long* fb;
+    cudaStream_t st;
+    template <class PP>
+    int operator()() {
+        return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
+            return build_op<Q, K, SS>(*pp, *sc, x0, X, N, Fe, ce, h, fb, st);
+        });
+    }
+};
+
+static int check_problem(const odx_problem* P, const odx_stepper* S) {
+    if (!P || !S) return fail(ODX_EINVAL, "null problem or stepper descriptor");
+    if (P->dim < 1 || P->dim > 64) return fail(ODX_EINVAL, "dim must be in [1, 64]");
+    if (P->problem_id < 0 || P->problem_id >= ODX_NUM_PROBLEMS)
+        return fail(ODX_EUNSUPPORTED, "unknown problem id (no device functor)");
+    return ODX_OK;
+}
+
+}  // namespace odx
+
+using namespace odx;
+
+extern "C" {
+
+int odx_abi_version(void) { return ODX_ABI_VERSION; }
+
+const char* odx_last_error(void) { return g_err.c_str(); }
+
+int odx_supported(const odx_problem* P, const odx_stepper* S) {
+    if (check_problem(P, S) != ODX_OK) return 0;
+    StepCoefs sc;
+    if (!fill_coefs(S, 1.0, sc)) return 0;
+    if (dense_supported(P, S)) return 1;
+    int r = with_small_problem(P->problem_id, P->dim, ProbeFn{S});
+    return r == 1 ? 1 : 0;
+}
+
+static int make_solve_params(const odx_problem* P, const odx_stepper* S, const double* x0,
+                             double* X, int64_t B, int64_t N, double dt, const odx_newton_cfg* C,
+                             double* hist, double* shist, int32_t* iters, int32_t* status,
+                             int64_t* sidx, SolveParams& p) {
+    int rc = check_problem(P, S);
+    if (rc) return rc;
+    if (!C || C->max_iters < 1) return fail(ODX_EINVAL, "max_iters must be at least 1");
+    if (C->residual_tol < 0.0 || C->step_tol < 0.0) return fail(ODX_EINVAL, "negative tolerance");
+    if (B < 1 || N < 1) return fail(ODX_EINVAL, "need B >= 1 and N >= 1");
+    if (!(dt > 0.0)) return fail(ODX_EINVAL, "dt must be positive");
+    std::memset(&p, 0, sizeof(p));
+    if (!fill_params(P, p.prob)) return fail(ODX_EINVAL, "bad problem parameters");
+    if (!fill_coefs(S, dt, p.sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
+    p.x0 = x0;
+    p.X = X;
+    p.B = B;
+    p.N = N;
+    p.max_iters = C->max_iters;
+    p.abort_nonfinite = C->abort_nonfinite;
+    p.rtol = C->residual_tol;
+    p.stol = C->step_tol;
+    p.hist = hist;
+    p.shist = shist;
+    p.iters = iters;
+    p.status = status;
+    p.sidx = reinterpret_cast<long long*>(sidx);
+    return ODX_OK;
+}
+
+static int solve_impl(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
+                      size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
+    if (dense_supported(P, S)) return dense_solve(P, S, p, ws, ws_bytes, st, query, need);
+    int rc = with_small_problem(P->problem_id, P->dim, SolveFn{S, &p, ws, ws_bytes, st, query, need});
+    if (rc == ODX_EUNSUPPORTED && odx_last_error()[0] == 0)
+        set_error("no device path for problem %d with dim %d", P->problem_id, P->dim);
+    if (rc == ODX_EINVAL) set_error("problem %d does not have dim %d", P->problem_id, P->dim);
+    return rc;
+}
+
+size_t odx_solve_workspace_bytes(const odx_problem* P, const odx_stepper* S, int64_t B,
+                                 int64_t N, const odx_newton_cfg* C) {
+    SolveParams p;
+    if (make_solve_params(P, S, nullptr, nullptr, B, N, 1.0, C, nullptr, nullptr, nullptr,
+                          nullptr, nullptr, p) != ODX_OK)
+        return 0;
+    size_t need = 0;
+    if (solve_impl(P, S, p, nullptr, 0, nullptr, true, &need) != ODX_OK) return 0;
+    return need;
+}
+
+int odx_solve(const odx_problem* P, const odx_stepper* S, const double* x0, double* X, int64_t B,
+              int64_t N, double dt, const odx_newton_cfg* C, double* hist, double* scaled_hist,
+              int32_t* iters, int32_t* status, int64_t* status_index, void* workspace,
+              size_t workspace_bytes, void* stream) {
+    g_err.clear();
+    SolveParams p;
+    int rc = make_solve_params(P, S, x0, X, B, N, dt, C, hist, scaled_hist, iters, status,
+                               status_index, p);
+    if (rc) return rc;
+    if (!x0 || !X || !iters || !status || !status_index)
+        return fail(ODX_EINVAL, "null device buffer");
+    return solve_impl(P, S, p, workspace, workspace_bytes, (cudaStream_t)stream, false, nullptr);
+}
+
+static int build_common(const odx_problem* P, const odx_stepper* S, int kind, const double* x0,
+                        const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,
+                        int64_t* first_bad, void* stream) {
+    g_err.clear();
+    int rc = check_problem(P, S);
+    if (rc) return rc;
+    if (S->kind != kind) return fail(ODX_EINVAL, "stepper kind does not match the build op");
+    if (N < 0) return fail(ODX_EINVAL, "N must be >= 0");
+    ProbParams pp;
+    StepCoefs sc;
+    if (!fill_params(P, pp)) return fail(ODX_EINVAL, "bad problem parameters");
+    if (!fill_coefs(S, dt, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
+    if (kind == ODX_STEP_IMPLICIT_WEIGHTED && !first_bad)
+        return fail(ODX_EINVAL, "first_bad must be a device int64 pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dense_supported(P, S))
+        return dense_build_op(P, S, sc, x0, X, N, Fe, ce, h,
+                              reinterpret_cast<long long*>(first_bad), st);
+    return with_small_problem(P->problem_id, P->dim,
+                              BuildFn{S, &pp, &sc, x0, X, N, Fe, ce, h,
+                                  reinterpret_cast<long long*>(first_bad), st});
+}
+
+int odx_build_explicit(const odx_problem* P, const odx_stepper* S, const double* x0,
+                       const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,
+                       void* stream) {
+    return build_common(P, S, ODX_STEP_EXPLICIT_RK, x0, X, N, dt, Fe, ce, h, nullptr, stream);
+}
+
+int odx_build_implicit(const odx_problem* P, const odx_stepper* S, const double* x0,
+                       const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,
+                       int64_t* first_bad, void* stream) {
+    return build_common(P, S, ODX_STEP_IMPLICIT_WEIGHTED, x0, X, N, dt, Fe, ce, h, first_bad,
+                        stream);
+}
+
+size_t odx_scan_affine_workspace_bytes(int64_t N, int32_t d) {
+    if (N < 0 || d < 1 || d > 64) return 0;
+    if (d > 4) return dense_scan_op_ws(N, d);
+    return scan_op_ws(N, d);
+}
+
+int odx_scan_affine(const double* Fin, const double* cin, int64_t N, int32_t d, double* Fp,
+                    double* cp, void* workspace, size_t workspace_bytes, void* stream) {
+    g_err.clear();
+    if (N < 0 || d < 1 || d > 64) return fail(ODX_EINVAL, "bad N or d");
+    if (d > 4)
+        return dense_scan_op(Fin, cin, N, d, Fp, cp, workspace, workspace_bytes,
+                             (cudaStream_t)stream);
+    return scan_op(Fin, cin, N, d, Fp, cp, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+int odx_max_abs(const double* A, int64_t n, int32_t d, double* out, void* stream) {
+    g_err.clear();
+    if (n < 0 || d < 1 || !out) return fail(ODX_EINVAL, "bad max_abs arguments");
+    return max_abs_op(A, n, d, out, (cudaStream_t)stream);
+}
+
+int odx_add_inplace(double* X, const double* U, int64_t n, int32_t d, void* stream) {
+    g_err.clear();
+    if (n < 0 || d < 1) return fail(ODX_EINVAL, "bad add_inplace arguments");
+    return add_op(X, U, n, d, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// common.cuh — host-side helpers shared by the ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/odescan_b200.h"
+#include "elements.cuh"
+
+namespace odx {
+
+void set_error(const char* fmt, ...);
+
+inline int fail(int code, const char* msg) {
+    set_error("%s", msg);
+    return code;
+}
+
+#define ODX_CUDA(call)                                                              \
+    do {                                                                            \
+        cudaError_t _e = (call);                                                    \
+        if (_e != cudaSuccess) {                                                    \
+            ::odx::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                             cudaGetErrorString(_e));                               \
+            return ODX_ECUDA;                                                       \
+        }                                                                           \
+    } while (0)
+
+int num_sms();
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Carves a workspace into aligned sub-buffers (dry run when base is null).
+struct Carver {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        off = align_up(off, 256);
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+bool fill_params(const odx_problem* P, ProbParams& pp);
+bool fill_coefs(const odx_stepper* S, double dt, StepCoefs& sc);
+void init_bad_slots(unsigned long long* red, int n, cudaStream_t st);
+
+}  // namespace odx

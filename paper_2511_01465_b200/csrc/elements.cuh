@@ -1,0 +1,306 @@
+// elements.cuh — per-step residual / scan-element construction in registers,
+// the affine element algebra, and the NaN-ignoring max-abs row rule.
+//
+// Reference: _kernels.py:261-342 (explicit RK elements with chain-ruled
+// tangents), :393-464 (implicit weighted elements with a pivoted LU per block),
+// :28-77 (LU), :84-95 (max_abs), affine_scan.py:64-78 (combine).
+#pragma once
+
+#include <cstdint>
+
+#include "problems.cuh"
+
+namespace odx {
+
+// ---------------------------------------------------------------------------
+// Step-map coefficients, precomputed on the host.  dta[i*S+j] = dt*a[i][j] is
+// the same double the reference forms inline (`dt * a[i, j] * kap`,
+// _kernels.py:271), so precomputing it changes no bits.
+// ---------------------------------------------------------------------------
+struct StepCoefs {
+    double dta[ODX_MAX_STAGES * ODX_MAX_STAGES];
+    double b[ODX_MAX_STAGES];
+    double dt;
+    double dt_wprev;  // dt * w_prev  (_kernels.py:455)
+    double dt_wnext;  // dt * w_next  (_kernels.py:430)
+    double w_prev, w_next;
+    int stages;
+};
+
+template <int D>
+struct Elem {
+    double F[D * D];
+    double c[D];
+};
+
+// combine(earlier e, later l) = (Fl Fe, Fl ce + cl)   affine_scan.py:64-78
+template <int D>
+__device__ __forceinline__ void compose(const Elem<D>& e, const Elem<D>& l, Elem<D>& o) {
+    Elem<D> t;
+#pragma unroll
+    for (int r = 0; r < D; r++) {
+        double acc = l.c[r];
+#pragma unroll
+        for (int q = 0; q < D; q++) acc += l.F[r * D + q] * e.c[q];
+        t.c[r] = acc;
+    }
+#pragma unroll
+    for (int r = 0; r < D; r++)
+#pragma unroll
+        for (int s = 0; s < D; s++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; q++) acc += l.F[r * D + q] * e.F[q * D + s];
+            t.F[r * D + s] = acc;
+        }
+    o = t;
+}
+
+// y = F z + c  (apply an element to a state offset)
+template <int D>
+__device__ __forceinline__ void apply(const Elem<D>& e, const double* z, double* y) {
+    double t[D];
+#pragma unroll
+    for (int r = 0; r < D; r++) {
+        double acc = e.c[r];
+#pragma unroll
+        for (int q = 0; q < D; q++) acc += e.F[r * D + q] * z[q];
+        t[r] = acc;
+    }
+#pragma unroll
+    for (int r = 0; r < D; r++) y[r] = t[r];
+}
+
+template <int D>
+__device__ __forceinline__ void set_identity(Elem<D>& e) {
+#pragma unroll
+    for (int r = 0; r < D; r++) {
+        e.c[r] = 0.0;
+#pragma unroll
+        for (int s = 0; s < D; s++) e.F[r * D + s] = (r == s) ? 1.0 : 0.0;
+    }
+}
+
+// Row rule of _kernels.max_abs (:84-95): loc takes v whenever !(v <= loc), so a
+// NaN replaces loc and is replaced again by the next entry; a row whose loc
+// ends NaN is dropped by the cross-row max (fmax drops NaN, like numba's
+// max(out, nan)).  Results are >= 0 or +inf, so their bit patterns order as
+// unsigned integers (atomicMax on the bits).
+template <int D>
+__device__ __forceinline__ double row_max_abs(const double* v) {
+    double loc = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+        double a = fabs(v[j]);
+        if (!(a <= loc)) loc = a;
+    }
+    return loc;
+}
+
+__device__ __forceinline__ double nan_drop_max(double acc, double loc) {
+    return fmax(acc, loc);  // fmax(acc, NaN) = acc
+}
+
+// ---------------------------------------------------------------------------
+// Explicit RK element for one step (_kernels.py:261-342).
+// prev = x0 (k == 0) or X[k-1]; xk = X[k].  Outputs element (F, c) with
+// F = I + dg/dx (0 for k == 0), c = -h, and the residual row h.
+// The stage loops run over every j < i including zero tableau entries, as the
+// reference does, so non-finite stages propagate identically.
+// ---------------------------------------------------------------------------
+template <class P, int S>
+__device__ __forceinline__ void build_explicit_step(const P& prob, const StepCoefs& sc,
+                                                    const double* prev, const double* xk,
+                                                    bool first, Elem<P::D>& el, double* h) {
+    constexpr int D = P::D;
+    double kap[S][D];
+    double dkap[S][D * D];
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        double xs[D];
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            double acc = prev[r];
+#pragma unroll
+            for (int j = 0; j < i; j++) acc += sc.dta[i * S + j] * kap[j][r];
+            xs[r] = acc;
+        }
+        prob.f(xs, kap[i]);
+        double Js[D * D];
+        prob.jac(xs, Js);
+        double M[D * D];
+#pragma unroll
+        for (int r = 0; r < D; r++)
+#pragma unroll
+            for (int c = 0; c < D; c++) {
+                double m = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int j = 0; j < i; j++) m += sc.dta[i * S + j] * dkap[j][r * D + c];
+                M[r * D + c] = m;
+            }
+#pragma unroll
+        for (int r = 0; r < D; r++)
+#pragma unroll
+            for (int c = 0; c < D; c++) {
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q < D; q++) acc += Js[r * D + q] * M[q * D + c];
+                dkap[i][r * D + c] = acc;
+            }
+    }
+#pragma unroll
+    for (int r = 0; r < D; r++) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < S; i++) acc += sc.b[i] * kap[i][r];
+        double g = sc.dt * acc;
+        double hv = xk[r] - prev[r] - g;
+        h[r] = hv;
+        el.c[r] = -hv;
+    }
+#pragma unroll
+    for (int r = 0; r < D; r++)
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < S; i++) acc += sc.b[i] * dkap[i][r * D + c];
+            double jg = sc.dt * acc;
+            el.F[r * D + c] = first ? 0.0 : jg + ((r == c) ? 1.0 : 0.0);
+        }
+}
+
+// ---------------------------------------------------------------------------
+// Register LU with partial pivoting (_kernels.py:28-77).  Row swaps are
+// expressed as predicated moves over compile-time indices so A stays in
+// registers.  Returns -1 or the first pivot index below the 1e-300 floor.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ int lu_factor_reg(double* A, int* piv) {
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+        int p = k;
+        double best = fabs(A[k * D + k]);
+#pragma unroll
+        for (int i = k + 1; i < D; i++) {
+            double v = fabs(A[i * D + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        if (best < 1e-300) return k;
+        piv[k] = p;
+#pragma unroll
+        for (int i = k + 1; i < D; i++) {
+            if (p == i) {
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    double t = A[k * D + j];
+                    A[k * D + j] = A[i * D + j];
+                    A[i * D + j] = t;
+                }
+            }
+        }
+        double inv = 1.0 / A[k * D + k];
+#pragma unroll
+        for (int i = k + 1; i < D; i++) {
+            double m = A[i * D + k] * inv;
+            A[i * D + k] = m;
+#pragma unroll
+            for (int j = k + 1; j < D; j++) A[i * D + j] -= m * A[k * D + j];
+        }
+    }
+    return -1;
+}
+
+template <int D>
+__device__ __forceinline__ void lu_solve_reg(const double* A, const int* piv, double* x) {
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+#pragma unroll
+        for (int i = k + 1; i < D; i++) {
+            if (piv[k] == i) { double t = x[k]; x[k] = x[i]; x[i] = t; }
+        }
+#pragma unroll
+        for (int i = k + 1; i < D; i++) x[i] -= A[i * D + k] * x[k];
+    }
+#pragma unroll
+    for (int i = D - 1; i >= 0; i--) {
+        double acc = x[i];
+#pragma unroll
+        for (int j = i + 1; j < D; j++) acc -= A[i * D + j] * x[j];
+        x[i] = acc / A[i * D + i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Implicit weighted element (_kernels.py:393-464):
+//   h = X[k] - prev - dt (w_p f(prev) + w_n f(X[k]))
+//   A = I - dt w_n J(X[k]);  c = A^{-1}(-h);  F = A^{-1}(I + dt w_p J(prev)), 0 at k=0
+// f and J are evaluated at prev even when w_prev = 0.  A singular
+// block gives F = c = 0 and returns true.
+// ---------------------------------------------------------------------------
+template <class P>
+__device__ __forceinline__ bool build_implicit_step(const P& prob, const StepCoefs& sc,
+                                                   const double* prev, const double* xk,
+                                                   bool first, Elem<P::D>& el, double* h) {
+    constexpr int D = P::D;
+    double fprev[D], fnext[D], Jp[D * D], A[D * D];
+    prob.f(prev, fprev);
+    prob.f(xk, fnext);
+    prob.jac(prev, Jp);
+    prob.jac(xk, A);
+#pragma unroll
+    for (int r = 0; r < D; r++)
+        h[r] = xk[r] - prev[r] - sc.dt * (sc.w_prev * fprev[r] + sc.w_next * fnext[r]);
+#pragma unroll
+    for (int r = 0; r < D; r++)
+#pragma unroll
+        for (int c = 0; c < D; c++)
+            A[r * D + c] = ((r == c) ? 1.0 : 0.0) - sc.dt_wnext * A[r * D + c];
+    int piv[D];
+    int st = lu_factor_reg<D>(A, piv);
+    if (st >= 0) {
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            el.c[r] = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; c++) el.F[r * D + c] = 0.0;
+        }
+        return true;
+    }
+    double col[D];
+#pragma unroll
+    for (int r = 0; r < D; r++) col[r] = -h[r];
+    lu_solve_reg<D>(A, piv, col);
+#pragma unroll
+    for (int r = 0; r < D; r++) el.c[r] = col[r];
+    if (first) {
+#pragma unroll
+        for (int i = 0; i < D * D; i++) el.F[i] = 0.0;
+    } else {
+#pragma unroll
+        for (int c = 0; c < D; c++) {
+#pragma unroll
+            for (int r = 0; r < D; r++) col[r] = sc.dt_wprev * Jp[r * D + c] + ((r == c) ? 1.0 : 0.0);
+            lu_solve_reg<D>(A, piv, col);
+#pragma unroll
+            for (int r = 0; r < D; r++) el.F[r * D + c] = col[r];
+        }
+    }
+    return false;
+}
+
+// Uniform entry used by the fused kernels: KIND 0 = explicit RK with S stages,
+// KIND 1 = implicit weighted.  Returns true for a singular implicit block.
+template <class P, int KIND, int S>
+__device__ __forceinline__ bool build_step(const P& prob, const StepCoefs& sc, const double* prev,
+                                           const double* xk, bool first, Elem<P::D>& el,
+                                           double* h) {
+    if constexpr (KIND == 0) {
+        build_explicit_step<P, S>(prob, sc, prev, xk, first, el, h);
+        return false;
+    } else {
+        return build_implicit_step<P>(prob, sc, prev, xk, first, el, h);
+    }
+}
+
+}  // namespace odx

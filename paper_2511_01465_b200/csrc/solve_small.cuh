@@ -1,0 +1,442 @@
+// solve_small.cuh — fused Newton-iteration kernels for small state dims (d <= 4).
+//
+// One Newton iteration of the reference (newton_pint.py:366-396) is
+//   build (_kernels.build_*) -> max_abs(h) -> scan_affine -> add_inplace,
+// four passes over HBM plus the scan's temporaries.  Here one pass does all
+// of it: the tile of X is staged in shared memory, every thread builds the
+// elements of ITEMS consecutive steps in registers, the block scans them, the
+// tile chains to its predecessors through a decoupled look-back, and
+// X_next = X + dx is written.  Only X is read and X_next written per
+// iteration (16*d bytes per step).  The Newton loop itself runs on the device:
+//
+//  * resident_solve_kernel — one CTA per trajectory (N <= THREADS*ITEMS), the
+//    whole solve in one launch with X resident in shared memory (BASELINE
+//    cfg 1 and the batched cfg 3).
+//  * persistent_solve_kernel — cooperative persistent grid for one long
+//    trajectory (cfg 2, cfg 5), tiles claimed in order from a per-iteration
+//    counter, X ping-ponged in HBM, a grid barrier and an identical
+//    on-device decision in every CTA after each iteration.
+//
+// The decision sequence is solve()'s (newton_pint.py:373-394) plus the
+// BASELINE step rule, identical to oracle/odescan_oracle.c:orc_solve.
+#pragma once
+
+#include <cstdint>
+
+#include "scan.cuh"
+
+namespace odx {
+
+struct SolveParams {
+    ProbParams prob;
+    StepCoefs sc;
+    const double* x0;  // B x D
+    double* X;         // B x N x D (guess in, final iterate out)
+    long long B, N;
+    int max_iters;
+    int abort_nonfinite;
+    double rtol, stol;
+    double* hist;   // B x (max_iters+1) or null
+    double* shist;  // B x (max_iters+1) or null
+    int* iters;
+    int* status;
+    long long* sidx;
+    // persistent-kernel workspace
+    double* Xalt;
+    uint32_t* flags;
+    double* aggbuf;
+    double* inclbuf;
+    uint32_t* ctr;
+    unsigned long long* red;  // 4 x (max_iters+1): rn, sc, step, bad
+    unsigned* bar;            // count, gen
+    long long ntiles;
+};
+
+struct Decision {
+    int stop;
+    int status;
+    long long index;
+    int iters;
+};
+
+// solve() decision sequence (newton_pint.py:373-394) + BASELINE step rule.
+__device__ __forceinline__ Decision decide(int it, const SolveParams& p, double rn,
+                                           unsigned long long bad, double step_prev) {
+    Decision d{0, -1, -1, 0};
+    if (bad != ~0ull) {
+        d.stop = 1; d.status = ODX_ST_SINGULAR; d.index = (long long)bad; d.iters = it;
+        return d;
+    }
+    if (isinf(rn) && p.abort_nonfinite) {
+        d.stop = 1; d.status = ODX_ST_NONFINITE; d.index = it; d.iters = it;
+        return d;
+    }
+    bool conv = (p.rtol > 0.0 && rn <= p.rtol) || (p.stol > 0.0 && it > 0 && step_prev < p.stol);
+    if (it >= p.max_iters) {
+        d.stop = 1; d.status = conv ? ODX_ST_CONVERGED : ODX_ST_MAXITER; d.iters = p.max_iters;
+        return d;
+    }
+    if (conv) {
+        d.stop = 1; d.status = ODX_ST_CONVERGED; d.iters = it;
+    }
+    return d;
+}
+
+// Shared-memory row staging with one pad double per ITEMS*D doubles, so that
+// thread t's rows start at an odd multiple of 8 bytes (no bank conflicts when
+// a warp reads its blocked rows).
+template <int D, int ITEMS>
+struct RowLayout {
+    static constexpr int CH = ITEMS * D;  // doubles per thread chunk
+    __device__ __forceinline__ static int idx(int linear) { return linear + linear / CH; }
+    static constexpr int size(int rows) { return rows * D + (rows * D) / CH + 1; }
+};
+
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+struct SmallEngine {
+    static constexpr int D = P::D;
+    static constexpr int NW = THREADS / 32;
+    static constexpr int T = THREADS * ITEMS;
+    using L = RowLayout<D, ITEMS>;
+    static constexpr int XS = L::size(T + 1);
+
+    struct Shared {
+        double xs[XS];
+        double wtF[NW][D * D];
+        double wtc[NW][D];
+        int wthas[NW];
+        double z[D];
+        double redd[3][NW];
+        unsigned long long redb[NW];
+        long long tile;
+    };
+
+    // Build the ITEMS elements of this thread from rows staged in sm.xs
+    // (row 0 = the state before step `base`).  Accumulates rn/sc/bad.
+    __device__ __forceinline__ static void build_items(const P& prob, const StepCoefs& sc,
+                                                       const Shared& sm, long long base,
+                                                       long long N, Elem<D> (&el)[ITEMS],
+                                                       double& rn, double& scn,
+                                                       unsigned long long& bad) {
+        const int tid = threadIdx.x;
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const int r = tid * ITEMS + i;
+            const long long k = base + r;
+            if (k < N) {
+                double prev[D], xk[D], h[D];
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    prev[j] = sm.xs[L::idx(r * D + j)];
+                    xk[j] = sm.xs[L::idx((r + 1) * D + j)];
+                }
+                bool sing = build_step<P, KIND, S>(prob, sc, prev, xk, k == 0, el[i], h);
+                rn = nan_drop_max(rn, row_max_abs<D>(h));
+                if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(el[i].c));
+                if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
+            }
+        }
+    }
+
+    // Fold this thread's items, scan the block, and leave the warp totals in
+    // shared memory.  Returns the thread inclusive aggregate (within its warp).
+    __device__ __forceinline__ static void block_scan(Shared& sm, long long base, long long N,
+                                                      const Elem<D> (&el)[ITEMS], Elem<D>& agg,
+                                                      bool& has) {
+        const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+        has = false;
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const long long k = base + tid * ITEMS + i;
+            if (k < N) {
+                if (has)
+                    compose<D>(agg, el[i], agg);
+                else {
+                    agg = el[i];
+                    has = true;
+                }
+            }
+        }
+        if (!has) set_identity<D>(agg);
+        warp_inclusive_scan<D>(agg, has, lane);
+        if (lane == 31) {
+#pragma unroll
+            for (int i = 0; i < D * D; i++) sm.wtF[w][i] = agg.F[i];
+#pragma unroll
+            for (int i = 0; i < D; i++) sm.wtc[w][i] = agg.c[i];
+            sm.wthas[w] = has ? 1 : 0;
+        }
+    }
+
+    // Tile aggregate = warp totals composed in order (one thread).
+    __device__ __forceinline__ static void tile_aggregate(const Shared& sm, Elem<D>& A, bool& A_has) {
+        A_has = false;
+#pragma unroll 1
+        for (int w = 0; w < NW; w++) {
+            if (!sm.wthas[w]) continue;
+            Elem<D> e;
+#pragma unroll
+            for (int i = 0; i < D * D; i++) e.F[i] = sm.wtF[w][i];
+#pragma unroll
+            for (int i = 0; i < D; i++) e.c[i] = sm.wtc[w][i];
+            if (A_has)
+                compose<D>(A, e, A);
+            else {
+                A = e;
+                A_has = true;
+            }
+        }
+    }
+
+    // Apply the scanned prefix: given the tile-exclusive state offset sm.z,
+    // compute dx for every item, write X + dx into sm.xs rows 1..T, and
+    // accumulate max|dx| (NaN-ignoring row rule).
+    __device__ __forceinline__ static void apply_items(Shared& sm, long long base, long long N,
+                                                       const Elem<D> (&el)[ITEMS],
+                                                       const Elem<D>& agg, bool has,
+                                                       double& step) {
+        const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+        double z[D];
+#pragma unroll
+        for (int r = 0; r < D; r++) z[r] = sm.z[r];
+        // warp-exclusive: warp totals 0..w-1 applied in order
+#pragma unroll 1
+        for (int q = 0; q < w; q++) {
+            if (!sm.wthas[q]) continue;
+            Elem<D> e;
+#pragma unroll
+            for (int i = 0; i < D * D; i++) e.F[i] = sm.wtF[q][i];
+#pragma unroll
+            for (int i = 0; i < D; i++) e.c[i] = sm.wtc[q][i];
+            apply<D>(e, z, z);
+        }
+        // lane-exclusive within the warp
+        Elem<D> ex;
+        shfl_up_elem<D>(agg, ex, 1);
+        bool exh = __shfl_up_sync(FULL, has, 1) && lane > 0;
+        if (exh) apply<D>(ex, z, z);
+#pragma unroll
+        for (int i = 0; i < ITEMS; i++) {
+            const int r = tid * ITEMS + i;
+            const long long k = base + r;
+            if (k < N) {
+                double dx[D];
+                apply<D>(el[i], z, dx);
+                step = nan_drop_max(step, row_max_abs<D>(dx));
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    z[j] = dx[j];
+                    sm.xs[L::idx((r + 1) * D + j)] += dx[j];
+                }
+            }
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Resident solve: one CTA per trajectory, N <= THREADS*ITEMS, X in smem.
+// ---------------------------------------------------------------------------
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+resident_solve_kernel(const SolveParams p) {
+    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
+    constexpr int D = P::D;
+    constexpr int NW = E::NW;
+    using L = typename E::L;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typename E::Shared& sm = *reinterpret_cast<typename E::Shared*>(smem_raw);
+    __shared__ double dec_rn, dec_sc;
+    __shared__ unsigned long long dec_bad;
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const long long b = blockIdx.x;
+    const long long N = p.N;
+    const P prob(p.prob);
+    double* Xb = p.X + b * N * D;
+    const int H = p.max_iters + 1;
+
+    for (int i = tid; i < (int)((N + 1) * D); i += THREADS) {
+        long long row = i / D - 1;
+        sm.xs[L::idx(i)] = (row < 0) ? p.x0[b * D + i] : Xb[i - D];
+    }
+    __syncthreads();
+
+    double step_prev = __longlong_as_double(0x7ff8000000000000ll);  // NaN
+    Decision dd{0, -1, -1, 0};
+    for (int it = 0; it <= p.max_iters; it++) {
+        Elem<D> el[ITEMS];
+        double rn = 0.0, scn = 0.0;
+        unsigned long long bad = ~0ull;
+        E::build_items(prob, p.sc, sm, 0, N, el, rn, scn, bad);
+        rn = warp_max_nan_drop(rn);
+        scn = warp_max_nan_drop(scn);
+        bad = warp_min_u64(bad);
+        if (lane == 0) { sm.redd[0][w] = rn; sm.redd[1][w] = scn; sm.redb[w] = bad; }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, c = 0.0;
+            unsigned long long m = ~0ull;
+            for (int q = 0; q < NW; q++) {
+                a = fmax(a, sm.redd[0][q]);
+                c = fmax(c, sm.redd[1][q]);
+                m = sm.redb[q] < m ? sm.redb[q] : m;
+            }
+            dec_rn = a; dec_sc = (KIND == 0) ? a : c; dec_bad = m;
+        }
+        __syncthreads();
+        const double rnb = dec_rn;
+        dd = decide(it, p, rnb, dec_bad, step_prev);
+        if (tid == 0 && dd.status != ODX_ST_SINGULAR) {
+            if (p.hist) p.hist[b * H + it] = rnb;
+            if (p.shist) p.shist[b * H + it] = dec_sc;
+        }
+        if (dd.stop) break;
+
+        Elem<D> agg;
+        bool has;
+        E::block_scan(sm, 0, N, el, agg, has);
+        if (tid == 0) {
+#pragma unroll
+            for (int r = 0; r < D; r++) sm.z[r] = 0.0;
+        }
+        __syncthreads();
+        double step = 0.0;
+        E::apply_items(sm, 0, N, el, agg, has, step);
+        step = warp_max_nan_drop(step);
+        if (lane == 0) sm.redd[2][w] = step;
+        __syncthreads();
+        double s = 0.0;
+        for (int q = 0; q < NW; q++) s = fmax(s, sm.redd[2][q]);
+        step_prev = s;
+        __syncthreads();
+    }
+    for (int i = tid; i < (int)(N * D); i += THREADS) Xb[i] = sm.xs[L::idx(i + D)];
+    if (tid == 0) {
+        p.iters[b] = dd.iters;
+        p.status[b] = dd.status;
+        p.sidx[b] = dd.index;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent cooperative solve for one long trajectory.
+// ---------------------------------------------------------------------------
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+persistent_solve_kernel(const SolveParams p) {
+    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
+    constexpr int D = P::D;
+    constexpr int NW = E::NW;
+    constexpr int T = E::T;
+    using L = typename E::L;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typename E::Shared& sm = *reinterpret_cast<typename E::Shared*>(smem_raw);
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const long long N = p.N;
+    const P prob(p.prob);
+    const unsigned nblocks = gridDim.x;
+    double* cur = p.X;
+    double* nxt = p.Xalt;
+    double step_prev = __longlong_as_double(0x7ff8000000000000ll);
+    Decision dd{0, -1, -1, 0};
+
+    for (int it = 0; it <= p.max_iters; it++) {
+        const bool do_scan = it < p.max_iters;
+        const uint32_t epoch = (uint32_t)it + 1u;
+        double rn = 0.0, scn = 0.0, step = 0.0;
+        unsigned long long bad = ~0ull;
+        while (true) {
+            if (tid == 0) sm.tile = (long long)atomicAdd(p.ctr + it, 1u);
+            __syncthreads();
+            const long long t = sm.tile;
+            if (t >= p.ntiles) break;
+            const long long base = t * T;
+            // stage rows base-1 .. base+T-1 (row 0 = halo / x0)
+            for (int i = tid; i < (T + 1) * D; i += THREADS) {
+                long long g = (base - 1) * D + i;  // linear index into X
+                double v;
+                if (g < 0)
+                    v = p.x0[i];
+                else if (g < N * D)
+                    v = __ldcg(cur + g);
+                else
+                    v = 0.0;
+                sm.xs[L::idx(i)] = v;
+            }
+            __syncthreads();
+            Elem<D> el[ITEMS];
+            E::build_items(prob, p.sc, sm, base, N, el, rn, scn, bad);
+            if (do_scan) {
+                Elem<D> agg;
+                bool has;
+                E::block_scan(sm, base, N, el, agg, has);
+                __syncthreads();
+                if (w == 0) {
+                    Elem<D> A;
+                    bool A_has = false;
+                    if (lane == 0) E::tile_aggregate(sm, A, A_has);
+                    lookback_vec<D>(t, epoch, A, A_has, p.flags, p.aggbuf, p.inclbuf, sm.z, lane);
+                }
+                __syncthreads();
+                E::apply_items(sm, base, N, el, agg, has, step);
+                __syncthreads();
+                for (int i = tid; i < T * D; i += THREADS) {
+                    long long g = base * D + i;
+                    if (g < N * D) nxt[g] = sm.xs[L::idx(i + D)];
+                }
+            }
+            __syncthreads();
+        }
+        // per-block reductions -> one atomic each
+        rn = warp_max_nan_drop(rn);
+        scn = warp_max_nan_drop(scn);
+        step = warp_max_nan_drop(step);
+        bad = warp_min_u64(bad);
+        if (lane == 0) {
+            sm.redd[0][w] = rn; sm.redd[1][w] = scn; sm.redd[2][w] = step; sm.redb[w] = bad;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, c = 0.0, s = 0.0;
+            unsigned long long m = ~0ull;
+            for (int q = 0; q < NW; q++) {
+                a = fmax(a, sm.redd[0][q]);
+                c = fmax(c, sm.redd[1][q]);
+                s = fmax(s, sm.redd[2][q]);
+                m = sm.redb[q] < m ? sm.redb[q] : m;
+            }
+            unsigned long long* red = p.red + 4ll * it;
+            if (a > 0.0) atomicMax(red + 0, dbits(a));
+            if (c > 0.0) atomicMax(red + 1, dbits(c));
+            if (s > 0.0) atomicMax(red + 2, dbits(s));
+            if (m != ~0ull) atomicMin(red + 3, m);
+        }
+        grid_barrier(p.bar, p.bar + 1, nblocks);
+        const unsigned long long* red = p.red + 4ll * it;
+        const double rnb = bitsd(__ldcg(red + 0));
+        const double scb = (KIND == 0) ? rnb : bitsd(__ldcg(red + 1));
+        const unsigned long long badb = __ldcg(red + 3);
+        dd = decide(it, p, rnb, badb, step_prev);
+        if (blockIdx.x == 0 && tid == 0 && dd.status != ODX_ST_SINGULAR) {
+            if (p.hist) p.hist[it] = rnb;
+            if (p.shist) p.shist[it] = scb;
+        }
+        if (dd.stop) break;
+        step_prev = bitsd(__ldcg(red + 2));
+        double* t2 = cur; cur = nxt; nxt = t2;
+    }
+    if (cur != p.X) {
+        const long long total = N * D;
+        for (long long i = (long long)blockIdx.x * THREADS + tid; i < total;
+             i += (long long)nblocks * THREADS)
+            p.X[i] = __ldcg(cur + i);
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        p.iters[0] = dd.iters;
+        p.status[0] = dd.status;
+        p.sidx[0] = dd.index;
+    }
+}
+
+}  // namespace odx

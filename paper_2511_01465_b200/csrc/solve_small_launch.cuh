@@ -1,0 +1,110 @@
+// solve_small_launch.cuh — host launchers of the fused small-d Newton solve
+// kernels (resident and persistent).  Instantiated per problem by the generated
+// translation units under csrc/gen/ (see paper_2511_01465_b200/build.py).
+#pragma once
+#include "common.cuh"
+#include "dispatch.cuh"
+#include "solve_small.cuh"
+
+namespace odx {
+
+namespace {
+
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+int launch_resident(SolveParams& p, cudaStream_t st) {
+    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
+    auto kern = resident_solve_kernel<P, KIND, S, THREADS, ITEMS>;
+    const size_t smem = sizeof(typename E::Shared);
+    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)p.B, THREADS, smem, st>>>(p);
+    ODX_CUDA(cudaGetLastError());
+    return ODX_OK;
+}
+
+// Workspace of the persistent solve: X ping-pong buffer, look-back flags and
+// payloads, per-iteration tile counters / reductions, grid-barrier words.
+template <int D>
+struct PersistLayout {
+    size_t total = 0, zero_off = 0, zero_bytes = 0;
+    size_t Xalt, flags, ctr, red, bar, aggbuf, inclbuf;
+    long long ntiles = 0;
+    PersistLayout(long long N, long long T, int max_iters) {
+        ntiles = (N + T - 1) / T;
+        Carver c{nullptr};
+        auto at = [&](size_t bytes) { c.off = align_up(c.off, 256); size_t o = c.off; c.off += bytes; return o; };
+        Xalt = at((size_t)N * D * sizeof(double));
+        zero_off = align_up(c.off, 256);
+        flags = at((size_t)ntiles * 4);
+        ctr = at(((size_t)max_iters + 1) * 4);
+        red = at(4 * ((size_t)max_iters + 1) * 8);
+        bar = at(2 * 4);
+        zero_bytes = c.off - zero_off;
+        aggbuf = at((size_t)ntiles * (D * D + D) * sizeof(double));
+        inclbuf = at((size_t)ntiles * D * sizeof(double));
+        total = c.off + 256;  // + alignment slack of the caller's base pointer
+    }
+};
+
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+int launch_persistent(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
+    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
+    constexpr int D = P::D;
+    auto kern = persistent_solve_kernel<P, KIND, S, THREADS, ITEMS>;
+    const PersistLayout<D> lay(p.N, (long long)THREADS * ITEMS, p.max_iters);
+    if (ws == nullptr || ws_bytes < lay.total)
+        return fail(ODX_EWORKSPACE, "workspace too small for persistent solve");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    p.Xalt = reinterpret_cast<double*>(base + lay.Xalt);
+    p.flags = reinterpret_cast<uint32_t*>(base + lay.flags);
+    p.ctr = reinterpret_cast<uint32_t*>(base + lay.ctr);
+    p.red = reinterpret_cast<unsigned long long*>(base + lay.red);
+    p.bar = reinterpret_cast<unsigned*>(base + lay.bar);
+    p.aggbuf = reinterpret_cast<double*>(base + lay.aggbuf);
+    p.inclbuf = reinterpret_cast<double*>(base + lay.inclbuf);
+    p.ntiles = lay.ntiles;
+    ODX_CUDA(cudaMemsetAsync(base + lay.zero_off, 0, lay.zero_bytes, st));
+    // "bad" slots (4th of each iteration's reduction quad) start at all-ones
+    init_bad_slots(p.red, p.max_iters + 1, st);
+    const size_t smem = sizeof(typename E::Shared);
+    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+    if (per_sm < 1) return fail(ODX_ECUDA, "persistent kernel cannot be resident");
+    long long grid = (long long)per_sm * num_sms();
+    if (grid > p.ntiles) grid = p.ntiles;
+    void* args[] = {&p};
+    ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(THREADS),
+                                         args, smem, st));
+    ODX_CUDA(cudaGetLastError());
+    return ODX_OK;
+}
+
+}  // namespace
+
+// Resident path when the whole trajectory fits one CTA; persistent otherwise.
+template <class P, int KIND, int S>
+int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
+                size_t* need) {
+    constexpr int D = P::D;
+    constexpr int RI = (D <= 3) ? 8 : 4;   // items per thread, resident
+    constexpr int PI = (D <= 2) ? 4 : 2;   // items per thread, persistent
+    const bool resident = p.N <= 256LL * RI;
+    if (query) {
+        *need = 0;
+        if (!resident) {
+            const long long T = (p.N < 128LL * PI * 296) ? 128 : 128LL * PI;
+            *need = PersistLayout<D>(p.N, T, p.max_iters).total;
+        }
+        return ODX_OK;
+    }
+    if (resident) {
+        if (p.N <= 128LL * RI) return launch_resident<P, KIND, S, 128, RI>(p, st);
+        return launch_resident<P, KIND, S, 256, RI>(p, st);
+    }
+    if (p.B != 1) return fail(ODX_EUNSUPPORTED, "batched solve needs N <= resident limit");
+    // small N: 1 item/thread keeps >= 2 tiles per SM; large N: PI items/thread
+    if (p.N < 128LL * PI * 296) return launch_persistent<P, KIND, S, 128, 1>(p, ws, ws_bytes, st);
+    return launch_persistent<P, KIND, S, 128, PI>(p, ws, ws_bytes, st);
+}
+
+}  // namespace odx

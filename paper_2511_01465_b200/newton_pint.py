@@ -1,0 +1,332 @@
+"""Parallel-in-time Newton solver on the B200.
+
+Drop-in for odescan.newton_pint (/root/reference/pkg/src/odescan/newton_pint.py):
+same types (Trajectory :80-116, NewtonConfig :119-138, SolveReport :141-158),
+same errors (:56-77), same n_steps_for / initial_guess conventions (:161-207)
+and the same solve(problem, stepper, dt, guess, config) signature and
+return/raise behaviour (:326-406).  The body is different: the whole Newton
+loop — build, residual norm, affine scan, update, stop test — runs on the GPU
+inside libodescan_b200.so (one launch per solve), and the host only moves the
+guess in and the result out.
+
+Additions (BASELINE): NewtonConfig.step_tol (stop once max|dx| of the last
+update < step_tol) and NewtonConfig.abort_on_nonfinite=False (fixed-iteration
+timing mode that keeps iterating through inf/NaN); solve_batch() for B
+independent trajectories with per-trajectory status.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .problems import OdeProblem
+from .steppers import StepperIncrement
+
+__all__ = [
+    "Trajectory", "NewtonConfig", "SolveReport", "BatchSolveReport",
+    "SingularDiagonalBlockError", "NonFiniteError", "n_steps_for", "initial_guess", "solve",
+    "solve_batch", "solve_device", "GUESS_POLICIES",
+]
+
+GUESS_POLICIES = ("ones", "zeros", "replicate_x0", "coarse_euler")
+
+
+class SingularDiagonalBlockError(Exception):
+    """A diagonal block I - dg/dx_next was singular to working precision (newton_pint.py:56-66)."""
+
+    def __init__(self, block_index: int):
+        self.block_index = int(block_index)
+        super().__init__(
+            f"diagonal block at time step {block_index} is singular to "
+            f"working precision; the implicit step is not locally solvable there")
+
+
+class NonFiniteError(Exception):
+    """The residual became NaN or infinite; the iteration is diverging (:69-77)."""
+
+    def __init__(self, iteration: int):
+        self.iteration = int(iteration)
+        super().__init__(f"non-finite values at iteration {iteration}; diverging")
+
+
+@dataclass
+class Trajectory:
+    """States x_1..x_N on a uniform grid plus the fixed x0 (newton_pint.py:80-116).
+
+    states may be a numpy array (host) or a CUDA torch tensor (device-resident
+    results of solve_device / output="torch").
+    """
+
+    x0: np.ndarray
+    states: object
+    dt: float
+    n_steps: int
+
+    def __post_init__(self):
+        self.x0 = np.asarray(self.x0, dtype=np.float64)
+        if not _is_torch(self.states):
+            self.states = np.asarray(self.states, dtype=np.float64)
+        if self.x0.ndim != 1:
+            raise ValueError("x0 must be 1-D")
+        shape = tuple(self.states.shape)
+        if len(shape) != 2 or shape[1] != self.x0.shape[0]:
+            raise ValueError(f"states must have shape (N, {self.x0.shape[0]}), got {shape}")
+        if shape[0] != self.n_steps:
+            raise ValueError(f"n_steps is {self.n_steps} but states has {shape[0]} rows")
+        if not self.dt >= 0.0:
+            raise ValueError(f"dt must be nonnegative, got {self.dt}")
+
+    @property
+    def dim(self) -> int:
+        return self.x0.shape[0]
+
+    def full_states(self) -> np.ndarray:
+        st = self.states.detach().cpu().numpy() if _is_torch(self.states) else self.states
+        return np.vstack([self.x0[None, :], st])
+
+
+@dataclass
+class NewtonConfig:
+    """Iteration controls (newton_pint.py:119-138) + BASELINE's step rule."""
+
+    max_iters: int = 11
+    residual_tol: float = 0.0
+    record_residuals: bool = True
+    step_tol: float = 0.0
+    abort_on_nonfinite: bool = True
+
+    def __post_init__(self):
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be at least 1")
+        if self.residual_tol < 0.0:
+            raise ValueError("residual_tol must be nonnegative")
+        if self.step_tol < 0.0:
+            raise ValueError("step_tol must be nonnegative")
+
+
+@dataclass
+class SolveReport:
+    """Outcome of a solve (newton_pint.py:141-158) + status fields."""
+
+    trajectory: Trajectory
+    residual_history: list
+    iterations_run: int
+    wall_time: float
+    scaled_residual_history: list = field(default_factory=list)
+    status: str = "maxiter"
+
+
+@dataclass
+class BatchSolveReport:
+    """Outcome of solve_batch: per-trajectory arrays (status codes are N.ST_*)."""
+
+    states: object            # (B, N, d) numpy or torch
+    residual_history: np.ndarray   # (B, max_iters+1), NaN where not reached
+    scaled_residual_history: np.ndarray
+    iterations_run: np.ndarray     # (B,)
+    status: np.ndarray             # (B,) int32
+    status_index: np.ndarray       # (B,) int64
+    wall_time: float
+
+
+_STATUS_NAMES = {N.ST_MAXITER: "maxiter", N.ST_CONVERGED: "converged",
+                 N.ST_NONFINITE: "nonfinite", N.ST_SINGULAR: "singular"}
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def n_steps_for(problem: OdeProblem, dt: float) -> int:
+    """Number of steps spanning [t0, tf]; dt must divide the interval (:161-171)."""
+    if not dt > 0.0:
+        raise ValueError(f"dt must be positive, got {dt}")
+    span = problem.tf - problem.t0
+    n = int(round(span / dt))
+    if n < 1 or abs(n * dt - span) > 1e-9:
+        raise ValueError(f"dt = {dt} does not divide the interval [{problem.t0}, {problem.tf}]")
+    return n
+
+
+def initial_guess(policy: str, problem: OdeProblem, n_steps: int) -> Trajectory:
+    """Starting iterate xi^(0) (newton_pint.py:174-207)."""
+    d = problem.dim
+    dt = (problem.tf - problem.t0) / n_steps
+    if policy == "ones":
+        states = np.ones((n_steps, d))
+    elif policy == "zeros":
+        states = np.zeros((n_steps, d))
+    elif policy == "replicate_x0":
+        states = np.tile(problem.x0, (n_steps, 1))
+    elif policy == "coarse_euler":
+        stride = max(1, n_steps // 100)
+        dt_coarse = stride * dt
+        states = np.empty((n_steps, d))
+        v = problem.x0.copy()
+        k = 0
+        while k < n_steps:
+            v = v + dt_coarse * problem.f(v)
+            hi = min(k + stride, n_steps)
+            states[k:hi] = v
+            k = hi
+    else:
+        raise ValueError(f"unknown initial-guess policy {policy!r}; "
+                         f"available: {', '.join(GUESS_POLICIES)}")
+    return Trajectory(problem.x0.copy(), states, dt, n_steps)
+
+
+def _resolve_guess(guess, problem: OdeProblem, n: int, dt: float) -> Trajectory:
+    if isinstance(guess, Trajectory):
+        if guess.n_steps != n or guess.dim != problem.dim:
+            raise ValueError(f"guess trajectory has {guess.n_steps} steps of dim {guess.dim}, "
+                             f"expected {n} of dim {problem.dim}")
+        return guess
+    return initial_guess(guess, problem, n)
+
+
+def _validate(problem: OdeProblem, stepper: StepperIncrement):
+    if stepper.problem is not problem:
+        raise ValueError("stepper was built for a different problem instance")
+    if problem.device is None:
+        raise ValueError(f"problem {problem.name!r} lacks a device functor, which solve() "
+                         f"requires (there is no CPU fallback)")
+    P = problem.native()
+    S = stepper.native()
+    if not N.lib().odx_supported(P, S):
+        raise ValueError(f"no compiled device path for problem {problem.name!r} "
+                         f"(dim {problem.dim}) with stepper {stepper.name!r}")
+    return P, S
+
+
+def _device(device):
+    import torch
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ValueError("the B200 solver runs on CUDA devices only")
+    return device
+
+
+def solve_device(P, S, x0, X, dt: float, config: NewtonConfig, *, stream=None):
+    """Run the native solve on device tensors (x0: (B, d), X: (B, N, d), fp64, CUDA).
+
+    X is overwritten with the final iterates.  Returns device tensors
+    (hist, shist, iters, status, status_index) without synchronising.
+    """
+    import torch
+    assert X.is_cuda and X.dtype == torch.float64 and X.is_contiguous()
+    B, n, d = X.shape
+    dev = X.device
+    H = config.max_iters + 1
+    hist = torch.full((B, H), float("nan"), dtype=torch.float64, device=dev)
+    shist = torch.full((B, H), float("nan"), dtype=torch.float64, device=dev)
+    iters = torch.zeros(B, dtype=torch.int32, device=dev)
+    status = torch.full((B,), -1, dtype=torch.int32, device=dev)
+    sidx = torch.full((B,), -1, dtype=torch.int64, device=dev)
+    cfg = N.make_cfg(config.max_iters, config.residual_tol, config.step_tol,
+                     config.abort_on_nonfinite)
+    L = N.lib()
+    ws_bytes = L.odx_solve_workspace_bytes(P, S, B, n, cfg)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    st = stream if stream is not None else N.stream_handle(dev)
+    N.check(L.odx_solve(P, S, N.ptr(x0), N.ptr(X), B, n, float(dt), cfg, N.ptr(hist),
+                        N.ptr(shist), N.ptr(iters), N.ptr(status), N.ptr(sidx), N.ptr(ws),
+                        ws_bytes, st))
+    return hist, shist, iters, status, sidx
+
+
+def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones",
+          config: NewtonConfig | None = None, *, device=None, output: str = "numpy"
+          ) -> SolveReport:
+    """Solve the rolled-out system by parallel Newton iterations (newton_pint.py:326-406).
+
+    Raises SingularDiagonalBlockError / NonFiniteError exactly where the
+    reference does.  wall_time covers guess construction, the host->device
+    copy, the device loop and the device->host copy of the result.
+    output="torch" keeps the trajectory on the device.
+    """
+    import torch
+    if config is None:
+        config = NewtonConfig()
+    P, S = _validate(problem, stepper)
+    n = n_steps_for(problem, dt)
+    dev = _device(device)
+
+    t_begin = time.perf_counter()
+    start = _resolve_guess(guess, problem, n, dt)
+    if _is_torch(start.states):
+        X = start.states.detach().to(device=dev, dtype=torch.float64).clone().contiguous()
+    else:
+        X = torch.from_numpy(np.ascontiguousarray(start.states, np.float64)).to(dev)
+    X = X.reshape(1, n, problem.dim)
+    x0 = torch.from_numpy(np.ascontiguousarray(problem.x0, np.float64)).to(dev).reshape(1, -1)
+    hist, shist, iters, status, sidx = solve_device(P, S, x0, X, dt, config)
+    small = torch.cat([iters.to(torch.int64), status.to(torch.int64), sidx]).cpu().tolist()
+    it_run, st, idx = int(small[0]), int(small[1]), int(small[2])
+    if st == N.ST_SINGULAR:
+        raise SingularDiagonalBlockError(idx)
+    if st == N.ST_NONFINITE:
+        raise NonFiniteError(idx)
+    if st < 0:
+        raise RuntimeError("device solve did not report a status")
+    h = hist[0, : it_run + 1].cpu().numpy()
+    sh = shist[0, : it_run + 1].cpu().numpy()
+    states = X[0] if output == "torch" else X[0].cpu().numpy()
+    wall = time.perf_counter() - t_begin
+    traj = Trajectory(problem.x0.copy(), states, dt, n)
+    rec = config.record_residuals
+    return SolveReport(trajectory=traj,
+                       residual_history=[float(v) for v in h] if rec else [],
+                       iterations_run=it_run, wall_time=wall,
+                       scaled_residual_history=[float(v) for v in sh] if rec else [],
+                       status=_STATUS_NAMES.get(st, str(st)))
+
+
+def solve_batch(problem: OdeProblem, stepper: StepperIncrement, dt: float, x0s, guess=None,
+                config: NewtonConfig | None = None, *, device=None, output: str = "numpy"
+                ) -> BatchSolveReport:
+    """B independent trajectories sharing (problem, stepper, dt).
+
+    x0s: (B, d) initial conditions.  guess: None (replicate each x0 — the
+    BASELINE constant-x0 guess), a (B, N, d) array/tensor, or a policy name
+    applied to every trajectory.  Never raises on divergence: per-trajectory
+    status codes (N.ST_*) and status_index are returned instead.
+    """
+    import torch
+    if config is None:
+        config = NewtonConfig()
+    P, S = _validate(problem, stepper)
+    n = n_steps_for(problem, dt)
+    dev = _device(device)
+    t_begin = time.perf_counter()
+    x0t = (x0s.detach().to(dev, torch.float64) if _is_torch(x0s)
+           else torch.from_numpy(np.ascontiguousarray(x0s, np.float64)).to(dev)).contiguous()
+    B, d = x0t.shape
+    if d != problem.dim:
+        raise ValueError(f"x0s has dim {d}, expected {problem.dim}")
+    if guess is None:
+        X = x0t[:, None, :].expand(B, n, d).contiguous()
+    elif isinstance(guess, str):
+        g = initial_guess(guess, problem, n).states
+        X = torch.from_numpy(g).to(dev)[None].expand(B, n, d).contiguous()
+    elif _is_torch(guess):
+        X = guess.detach().to(dev, torch.float64).clone().contiguous()
+    else:
+        X = torch.from_numpy(np.array(guess, np.float64)).to(dev).contiguous()
+    if tuple(X.shape) != (B, n, d):
+        raise ValueError(f"guess has shape {tuple(X.shape)}, expected {(B, n, d)}")
+    hist, shist, iters, status, sidx = solve_device(P, S, x0t, X, dt, config)
+    torch.cuda.synchronize(dev)
+    rep = BatchSolveReport(
+        states=X if output == "torch" else X.cpu().numpy(),
+        residual_history=hist.cpu().numpy(), scaled_residual_history=shist.cpu().numpy(),
+        iterations_run=iters.cpu().numpy(), status=status.cpu().numpy(),
+        status_index=sidx.cpu().numpy(), wall_time=0.0)
+    rep.wall_time = time.perf_counter() - t_begin
+    return rep

@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (north_star): iterates agree to max|x_gpu - x_ref| <= 1e-9 *
+max(1, max|x_ref|) over entries finite in the reference, non-finite row masks
+agree, statuses agree and iteration counts agree within +-1.  Kernel-level ops
+use tighter bounds (FMA contraction and scan association are the only
+arithmetic differences from the reference).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from _refcases import BUILD_SPECS, REF_PROBLEMS, guess_array, n_steps
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def scaled_close(x, ref, tol=TOL, what=""):
+    x = np.asarray(x)
+    ref = np.asarray(ref)
+    assert x.shape == ref.shape, (what, x.shape, ref.shape)
+    fin_ref = np.isfinite(ref)
+    rows_ref = fin_ref.reshape(ref.shape[0], -1).all(axis=1) if ref.ndim > 1 else fin_ref
+    rows_x = (np.isfinite(x).reshape(x.shape[0], -1).all(axis=1) if x.ndim > 1
+              else np.isfinite(x))
+    assert np.array_equal(rows_ref, rows_x), (
+        f"{what}: non-finite row masks differ ({(rows_ref != rows_x).sum()} rows, first "
+        f"{np.argmax(rows_ref != rows_x)})")
+    if not fin_ref.any():
+        return 0.0
+    scale = max(1.0, float(np.max(np.abs(ref[fin_ref]))))
+    err = float(np.max(np.abs(x[fin_ref] - ref[fin_ref])))
+    assert err <= tol * scale, f"{what}: max err {err:.3e} > {tol:.1e} * {scale:.3e}"
+    return err / scale
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda()
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2511_01465_b200 as P
+    from paper_2511_01465_b200 import _native
+    _native.lib()
+    assert torch.cuda.is_available()
+    return P
+
+
+def _ref_problem(P, name):
+    if name == "cartpole_sq":
+        return P.cart_pole(centripetal_term=True)
+    return P.get_problem(name)
+
+
+def _build_problem(P, name):
+    pid, d, params = BUILD_SPECS[name]
+    if name in ("lorenz63",):
+        return P.lorenz63()
+    if name == "vdp10":
+        return P.van_der_pol(mu=10.0)
+    if name == "allen_cahn":
+        return P.allen_cahn()
+    return _ref_problem(P, name)
+
+
+# ---------------------------------------------------------------- ops ------
+
+@pytest.mark.parametrize("name", [n for n in BUILD_SPECS if n != "allen_cahn"])
+def test_build_ops_vs_golden(pkg, golden_kernels, name):
+    from paper_2511_01465_b200 import kernels as K
+    g = golden_kernels
+    prob = _build_problem(pkg, name)
+    for sname in ("rk4", "euler"):
+        key = f"bx_{name}_{sname}"
+        st = pkg.get_stepper(sname, prob)
+        Fe, ce, h = K.build_explicit(prob, st, dev(g[key + "_x0"]), dev(g[key + "_X"]),
+                                     float(g[key + "_dt"]))
+        for got, ref in ((h, g[key + "_h"]), (ce, g[key + "_ce"]), (Fe, g[key + "_Fe"])):
+            scaled_close(got.cpu().numpy(), ref, 1e-13, key)
+    for sname, stname in (("be", "backward_euler"), ("trap", "trapezoidal")):
+        key = f"bi_{name}_{sname}"
+        st = pkg.get_stepper(stname, prob)
+        Fe, ce, h, bad = K.build_implicit(prob, st, dev(g[key + "_x0"]), dev(g[key + "_X"]),
+                                          float(g[key + "_dt"]))
+        assert bad == int(g[key + "_bad"])
+        for got, ref in ((h, g[key + "_h"]), (ce, g[key + "_ce"]), (Fe, g[key + "_Fe"])):
+            scaled_close(got.cpu().numpy(), ref, 1e-12, key)
+
+
+def test_build_implicit_nan_leak_and_singular(pkg, golden_kernels):
+    from paper_2511_01465_b200 import kernels as K
+    g = golden_kernels
+    prob = pkg.van_der_pol(mu=10.0)
+    Fe, ce, h, bad = K.build_implicit(prob, pkg.get_stepper("backward_euler", prob),
+                                      dev([2.0, 0.0]), dev(g["bi_leak_X"]), 1e-3)
+    assert bad == int(g["bi_leak_bad"])
+    assert np.array_equal(np.isnan(Fe.cpu().numpy()), np.isnan(g["bi_leak_Fe"]))
+    assert np.array_equal(np.isnan(h.cpu().numpy()), np.isnan(g["bi_leak_h"]))
+    sq = pkg.problems.square()
+    Fe, ce, h, bad = K.build_implicit(sq, pkg.get_stepper("backward_euler", sq), dev([1.0]),
+                                      dev(g["bi_sing_X"]), 0.1)
+    assert bad == 0
+
+
+def test_scan_op_reference_sizes(pkg, golden_kernels):
+    from paper_2511_01465_b200 import kernels as K
+    g = golden_kernels
+    for n in (1, 2, 5, 33, 256):
+        Fp, cp = K.scan_affine(dev(g[f"scan_n{n}_F"]), dev(g[f"scan_n{n}_c"]))
+        scaled_close(Fp.cpu().numpy(), g[f"scan_n{n}_Fp"], 1e-10, f"Fp n={n}")
+        scaled_close(cp.cpu().numpy(), g[f"scan_n{n}_cp"], 1e-10, f"cp n={n}")
+    for d in (1, 2, 4):
+        Fp, cp = K.scan_affine(dev(g[f"scand{d}_F"]), dev(g[f"scand{d}_c"]))
+        scaled_close(Fp.cpu().numpy(), g[f"scand{d}_Fp"], 1e-10, f"Fp d={d}")
+        scaled_close(cp.cpu().numpy(), g[f"scand{d}_cp"], 1e-10, f"cp d={d}")
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4])
+@pytest.mark.parametrize("n", [255, 256, 257, 70001])
+def test_scan_op_vs_oracle_large(pkg, oracle, d, n):
+    from paper_2511_01465_b200 import kernels as K
+    rng = np.random.default_rng(7 * n + d)
+    F = rng.standard_normal((n, d, d)) * (0.9 / math.sqrt(d))
+    c = rng.standard_normal((n, d))
+    Fp_r, cp_r = oracle.scan_affine(F, c)
+    Fp, cp = K.scan_affine(dev(F), dev(c))
+    scaled_close(cp.cpu().numpy(), cp_r, 1e-10, "cp")
+    scaled_close(Fp.cpu().numpy(), Fp_r, 1e-10, "Fp")
+
+
+def test_max_abs_and_add_ops(pkg, golden_kernels):
+    from paper_2511_01465_b200 import kernels as K
+    g = golden_kernels
+    i = 0
+    while f"maxabs{i}_A" in g:
+        assert K.max_abs(dev(g[f"maxabs{i}_A"])) == float(g[f"maxabs{i}_out"]), i
+        i += 1
+    X = dev(np.arange(12.0).reshape(6, 2))
+    K.add_inplace(X, dev(np.ones((6, 2))))
+    assert np.array_equal(X.cpu().numpy(), np.arange(12.0).reshape(6, 2) + 1)
+
+
+# -------------------------------------------------------------- solve ------
+
+def _oracle_ref_solve(oracle, name, sname, dt, policy, iters, **kw):
+    pid, d, params, x0, t0, tf = REF_PROBLEMS[name]
+    n = n_steps(t0, tf, dt)
+    return oracle.solve(pid, params, oracle.stepper_by_name(sname), x0,
+                        guess_array(policy, x0, n), dt, iters, **kw)
+
+
+@pytest.mark.parametrize("case", [
+    ("logistic", "rk4", 1e-2, "ones", 11), ("vdp", "rk4", 1e-2, "ones", 11),
+    ("cartpole", "rk4", 1e-2, "zeros", 11), ("dahlquist", "backward_euler", 0.1, "zeros", 5),
+    ("robertson", "backward_euler", 0.1, "zeros", 25), ("vdp", "trapezoidal", 1e-2, "ones", 8),
+    ("dahlquist", "euler", 1e-3, "ones", 1), ("logistic", "euler", 0.1, "ones", 3),
+    ("logistic", "rk4", 1e-5, "ones", 11),  # N = 1e6: persistent multi-CTA path
+])
+def test_solve_reference_problems(pkg, oracle, golden_solves, case):
+    name, sname, dt, policy, iters = case
+    prob = _ref_problem(pkg, name)
+    st = pkg.get_stepper(sname, prob)
+    rep = pkg.solve(prob, st, dt, policy, pkg.NewtonConfig(max_iters=iters))
+    ref = _oracle_ref_solve(oracle, name, sname, dt, policy, iters)
+    assert rep.iterations_run == ref["iters"] == iters
+    scaled_close(np.array(rep.residual_history), ref["hist"], 1e-7, "hist")
+    scaled_close(rep.trajectory.states, ref["X"], TOL, "states")
+
+
+def test_solve_residual_rule_and_errors(pkg, oracle):
+    prob = pkg.get_problem("logistic")
+    st = pkg.get_stepper("rk4", prob)
+    rep = pkg.solve(prob, st, 0.1, "ones", pkg.NewtonConfig(max_iters=20, residual_tol=1e-6))
+    ref = _oracle_ref_solve(oracle, "logistic", "rk4", 0.1, "ones", 20, residual_tol=1e-6)
+    assert abs(rep.iterations_run - ref["iters"]) <= 1
+    assert rep.residual_history[-1] <= 1e-6
+    assert len(rep.residual_history) == rep.iterations_run + 1
+    e = pkg.problems.exp_growth()
+    with pytest.raises(pkg.NonFiniteError) as ei:
+        pkg.solve(e, pkg.get_stepper("euler", e), 0.25,
+                  pkg.Trajectory(e.x0.copy(), np.full((4, 1), 800.0), 0.25, 4),
+                  pkg.NewtonConfig(max_iters=3))
+    assert ei.value.iteration == 0
+    sq = pkg.problems.square()
+    with pytest.raises(pkg.SingularDiagonalBlockError) as ei:
+        pkg.solve(sq, pkg.get_stepper("backward_euler", sq), 0.1,
+                  pkg.Trajectory(sq.x0.copy(), np.full((10, 1), 5.0), 0.1, 10),
+                  pkg.NewtonConfig(max_iters=2))
+    assert ei.value.block_index == 0
+
+
+def test_solve_converges_to_sequential(pkg, oracle):
+    """test_acceptance.py crit 5 pattern: converged Newton == sequential stepping."""
+    prob = pkg.get_problem("logistic")
+    st = pkg.get_stepper("rk4", prob)
+    rep = pkg.solve(prob, st, 1e-2, "ones", pkg.NewtonConfig(max_iters=11))
+    seq = oracle.seq_explicit(0, (1.0, 1.0), oracle.RK4_A, oracle.RK4_B, prob.x0, 1e-2, 1000)
+    assert np.max(np.abs(rep.trajectory.states - seq)) <= 1e-10
+    prob = pkg.get_problem("dahlquist")
+    st = pkg.get_stepper("backward_euler", prob)
+    rep = pkg.solve(prob, st, 0.1, "zeros", pkg.NewtonConfig(max_iters=5))
+    seq, code = oracle.seq_implicit(4, (-1000.0,), 0.0, 1.0, prob.x0, 0.1, 40)
+    assert code == -1
+    assert np.max(np.abs(rep.trajectory.states - seq)) <= 1e-12
+
+
+# ----------------------------------------------------- BASELINE configs ----
+
+def _cfg_problem(pkg, cfg):
+    if cfg.problem == "lorenz63":
+        return pkg.lorenz63(*cfg.params, x0=cfg.x0s()[0], tf=cfg.n_steps * cfg.dt)
+    if cfg.problem == "vdp":
+        return pkg.van_der_pol(mu=cfg.params[0], x0=cfg.x0s()[0], tf=cfg.n_steps * cfg.dt)
+    return pkg.allen_cahn(n=cfg.dim, eps=cfg.params[0], dx=cfg.params[1], u0=cfg.x0s()[0],
+                          tf=cfg.n_steps * cfg.dt)
+
+
+def _gpu_cfg_solve(pkg, cfg, n=None, max_iters=None, step_tol=None, abort=None, B=None):
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    n = cfg.n_steps if n is None else n
+    prob = _cfg_problem(pkg, cfg)
+    prob = type(prob)(**{**prob.__dict__, "tf": n * cfg.dt})
+    st = pkg.get_stepper(cfg.stepper, prob)
+    x0s = cfg.x0s() if B is None else cfg.x0s()[:B]
+    conf = pkg.NewtonConfig(max_iters=cfg.max_iters if max_iters is None else max_iters,
+                            step_tol=cfg.step_tol if step_tol is None else step_tol,
+                            abort_on_nonfinite=cfg.abort_nonfinite if abort is None else abort)
+    return solve_batch(prob, st, cfg.dt, x0s, None, conf)
+
+
+def test_cfg1_lorenz(pkg, golden_baseline):
+    from paper_2511_01465_b200.configs import CONFIGS
+    g = golden_baseline
+    cfg = CONFIGS[1]
+    r = _gpu_cfg_solve(pkg, cfg)
+    assert int(r.status[0]) == int(g["cfg1_status"])
+    assert abs(int(r.status_index[0]) - int(g["cfg1_index"])) <= 1
+    r1 = _gpu_cfg_solve(pkg, cfg, max_iters=1, step_tol=0.0, abort=False)
+    scaled_close(r1.states[0], g["cfg1_X1"], TOL, "iterate 1")
+    r3 = _gpu_cfg_solve(pkg, cfg, max_iters=3, step_tol=0.0, abort=False)
+    scaled_close(r3.states[0], g["cfg1_fixed3_X"], TOL, "iterate 3")
+
+
+def test_cfg2_vdp_be(pkg, golden_baseline):
+    from paper_2511_01465_b200.configs import CONFIGS
+    g = golden_baseline
+    cfg = CONFIGS[2]
+    r = _gpu_cfg_solve(pkg, cfg)
+    assert int(r.status[0]) == int(g["cfg2_status"])
+    assert abs(int(r.status_index[0]) - int(g["cfg2_index"])) <= 1
+    for k, key in ((1, "cfg2_X1_sub"), (2, "cfg2_X2_sub")):
+        rk = _gpu_cfg_solve(pkg, cfg, max_iters=k, step_tol=0.0, abort=False)
+        scaled_close(rk.states[0][::16], g[key], TOL, f"iterate {k}")
+    r4 = _gpu_cfg_solve(pkg, cfg, n=4096, max_iters=4, step_tol=0.0, abort=False)
+    scaled_close(r4.states[0], g["cfg2s_X"], TOL, "N=4096 iterate 4")
+
+
+def test_cfg3_batch(pkg, golden_baseline):
+    from paper_2511_01465_b200.configs import CONFIGS
+    g = golden_baseline
+    cfg = CONFIGS[3]
+    r = _gpu_cfg_solve(pkg, cfg)
+    assert np.array_equal(r.status, g["cfg3_status"])
+    assert np.all(np.abs(r.status_index - g["cfg3_index"]) <= 1)
+    assert np.all(np.abs(r.iterations_run - g["cfg3_iters"]) <= 1)
+    scaled_close(r.residual_history[:, 0], g["cfg3_hist0"], 1e-12, "hist0")
+    r1 = _gpu_cfg_solve(pkg, cfg, max_iters=1, step_tol=0.0, abort=False, B=4)
+    for b in range(4):
+        scaled_close(r1.states[b], g[f"cfg3_b{b}_X1"], TOL, f"b{b} iterate 1")
+
+
+def test_cfg5_vdp_rk4_fixed10_small(pkg, golden_baseline):
+    from paper_2511_01465_b200.configs import CONFIGS
+    g = golden_baseline
+    cfg = CONFIGS[5]
+    r = _gpu_cfg_solve(pkg, cfg, n=65536)
+    assert int(r.status[0]) == 0 and int(r.iterations_run[0]) == 10
+    fin = np.isfinite(r.states[0]).all(axis=1)
+    assert fin.sum() == int(g["cfg5s_finite_rows"])
+    scaled_close(r.states[0][::64], g["cfg5s_X_sub"], TOL, "iterate 10")
+    for k, key in ((1, "cfg5s_X1_sub"), (2, "cfg5s_X2_sub")):
+        rk = _gpu_cfg_solve(pkg, cfg, n=65536, max_iters=k)
+        scaled_close(rk.states[0][::64], g[key], TOL, f"iterate {k}")
