@@ -1,0 +1,521 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 parallel-in-time Newton solver (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+                    [--impl ours|reference]
+
+Metric: Newton time-steps/s = (trajectories x N steps x Newton iterations) / s.
+
+Workload (config.workload): BASELINE.json configs[1] = cfg2, van der Pol
+mu=10, backward Euler, N=65536, d=2, fp64.  One bench step = one solve of that
+trajectory running a FIXED 10 Newton iterations in the non-aborting timing
+mode (under BASELINE's own stop rule cfg2 ends NONFINITE after 2
+updates, so the stable steps/s figure is taken at a fixed iteration count; the
+stop-rule solve is timed too and reported under "stop_rule").  Inputs are
+resident in HBM when the timed region starts; L2 (126 MB) is flushed between
+steps because the 1 MB state would otherwise stay cached across solves.  Each
+step is timed with its own CUDA-event pair on the launching stream.
+
+Every other BASELINE config is measured the same way and reported under
+"configs" (cfg5 at N=2^26 is the HBM-scale case).
+
+--impl reference times the reference's CPU implementation of the path — the
+C restatement in oracle/ (bit-identical to the numba reference, see
+tests/test_oracle_golden.py) on all host cores — on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+PEAKS = REPO / "MEASURED_PEAKS.json"
+FP64_PEAK = REPO / "profiles" / "fp64_peak.json"
+
+# Algorithmic work per step per Newton iteration:
+# bytes = 16*d (x read once, x_new written once); flops by the counting
+# convention there (FMA = 2, tableau zeros removed, Jacobians dense).
+ALG = {
+    1: dict(bytes=48, flops=462),
+    2: dict(bytes=32, flops=71),
+    3: dict(bytes=48, flops=462),
+    4: dict(bytes=1024, flops=1238752),
+    5: dict(bytes=32, flops=210),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters", type=int, default=10, help="fixed Newton iterations per step")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-extra", action="store_true", help="skip the other-config lines")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# --------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/odx_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.2)
+        self.proc.terminate()
+        self.proc.wait()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxs.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        top = max(sms)
+        loaded = [s for s in sms if s >= 0.5 * top] or sms
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(maxs),
+                "samples": len(sms), "reasons": sorted(reasons)}
+
+
+def peaks():
+    hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
+    if PEAKS.exists():
+        try:
+            hbm = float(json.loads(PEAKS.read_text())["hbm_gbs"])
+            src = "measured (MEASURED_PEAKS.json)"
+        except (KeyError, ValueError):
+            pass
+    fp64, fsrc = 37000.0, "nominal datasheet (not measured)"
+    if FP64_PEAK.exists():
+        try:
+            fp64 = float(json.loads(FP64_PEAK.read_text())["dfma_gflops"])
+            fsrc = "measured (profiles/fp64_peak.json, DFMA)"
+        except (KeyError, ValueError):
+            pass
+    return hbm, src, fp64, fsrc
+
+
+# --------------------------------------------------------------------------
+# workloads
+# --------------------------------------------------------------------------
+def cfg_id(name: str) -> int:
+    return int(name.replace("cfg", ""))
+
+
+class Workload:
+    """Device-resident inputs of one BASELINE config + the native solve call."""
+
+    def __init__(self, cid: int, iters: int, n_override=None, batch_override=None, rank=0,
+                 world=1):
+        import torch
+        from paper_2511_01465_b200 import _native as N
+        from paper_2511_01465_b200.configs import CONFIGS
+        import paper_2511_01465_b200 as pkg
+        self.torch, self.N = torch, N
+        self.cfg = cfg = CONFIGS[cid]
+        self.cid = cid
+        self.n = n_override or cfg.n_steps
+        x0s = cfg.x0s()
+        if batch_override:
+            x0s = x0s[:batch_override]
+        if cid == 3 and world > 1:  # batch sharding: contiguous B/world per rank
+            per = (x0s.shape[0] + world - 1) // world
+            x0s = x0s[rank * per:(rank + 1) * per]
+        self.B = x0s.shape[0]
+        self.d = cfg.dim
+        if cfg.problem == "lorenz63":
+            prob = pkg.lorenz63(*cfg.params, x0=x0s[0], tf=self.n * cfg.dt)
+        elif cfg.problem == "vdp":
+            prob = pkg.van_der_pol(mu=cfg.params[0], x0=x0s[0], tf=self.n * cfg.dt)
+        else:
+            prob = pkg.allen_cahn(n=cfg.dim, eps=cfg.params[0], dx=cfg.params[1], u0=x0s[0],
+                                  tf=self.n * cfg.dt)
+        self.prob = prob
+        self.stepper = pkg.get_stepper(cfg.stepper, prob)
+        self.P, self.S = prob.native(), self.stepper.native()
+        self.iters = iters
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        self.x0 = torch.from_numpy(np.ascontiguousarray(x0s)).to(dev)
+        self.guess = self.x0[:, None, :].expand(self.B, self.n, self.d).contiguous()
+        self.X = torch.empty_like(self.guess)
+        self.host_guess = np.ascontiguousarray(self.guess[0].cpu().numpy())
+        self.set_mode(fixed=True)
+
+    def set_mode(self, fixed: bool):
+        torch, N = self.torch, self.N
+        if fixed:
+            self.ncfg = N.make_cfg(self.iters, 0.0, 0.0, False)
+            H = self.iters + 1
+        else:
+            self.ncfg = N.make_cfg(self.cfg.max_iters, 0.0, self.cfg.step_tol,
+                                   self.cfg.abort_nonfinite)
+            H = self.cfg.max_iters + 1
+        self.H = H
+        self.hist = torch.empty((self.B, H), dtype=torch.float64, device=self.dev)
+        self.shist = torch.empty_like(self.hist)
+        self.iters_t = torch.empty(self.B, dtype=torch.int32, device=self.dev)
+        self.status = torch.empty(self.B, dtype=torch.int32, device=self.dev)
+        self.sidx = torch.empty(self.B, dtype=torch.int64, device=self.dev)
+        L = N.lib()
+        self.ws_bytes = L.odx_solve_workspace_bytes(self.P, self.S, self.B, self.n, self.ncfg)
+        self.ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=self.dev)
+
+    def reset(self):
+        self.X.copy_(self.guess)
+
+    def launch(self):
+        N = self.N
+        N.check(N.lib().odx_solve(self.P, self.S, N.ptr(self.x0), N.ptr(self.X), self.B,
+                                  self.n, float(self.cfg.dt), self.ncfg, N.ptr(self.hist),
+                                  N.ptr(self.shist), N.ptr(self.iters_t), N.ptr(self.status),
+                                  N.ptr(self.sidx), N.ptr(self.ws), self.ws_bytes,
+                                  N.stream_handle(self.dev)))
+
+    def outcome(self):
+        it = self.iters_t.cpu().numpy()
+        st = self.status.cpu().numpy()
+        ix = self.sidx.cpu().numpy()
+        return it, st, ix
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # 256 MB written > 126 MB L2
+
+
+def time_steps(w: Workload, steps: int, warmup: int, flush):
+    torch = w.torch
+    for _ in range(warmup):
+        w.reset()
+        flush()
+        w.launch()
+    torch.cuda.synchronize()
+    durs = []
+    l0 = w.N.lib().odx_launch_count()
+    evs = []
+    for _ in range(steps):
+        w.reset()
+        flush()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        w.launch()
+        e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    launches = w.N.lib().odx_launch_count() - l0
+    durs = [a.elapsed_time(b) for a, b in evs]
+    return durs, launches
+
+
+def e2e_steps(w: Workload, steps: int, warmup: int):
+    """Same metric through the public API with HOST buffers: solve_batch(numpy)."""
+    torch = w.torch
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    conf = pkg.NewtonConfig(max_iters=w.iters, abort_on_nonfinite=False)
+    x0_host = w.x0.cpu().numpy()
+    guess_host = np.ascontiguousarray(np.broadcast_to(w.host_guess, (w.B, w.n, w.d)))
+    for _ in range(warmup):
+        solve_batch(w.prob, w.stepper, w.cfg.dt, x0_host, guess_host, conf)
+    torch.cuda.synchronize()
+    durs = []
+    for _ in range(steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep = solve_batch(w.prob, w.stepper, w.cfg.dt, x0_host, guess_host, conf)
+        e1.record()
+        torch.cuda.synchronize()
+        durs.append(e0.elapsed_time(e1))
+    h2d = guess_host.nbytes + x0_host.nbytes
+    d2h = rep.states.nbytes + rep.residual_history.nbytes * 2 + w.B * (4 + 4 + 8)
+    return durs, h2d, d2h
+
+
+def reduce_max(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def roofline_for(cid, n, B, iters, avg_ms, hbm, hbm_src, fp64, fp64_src):
+    alg = ALG[cid]
+    steps = n * B
+    # per launch: `iters` fused iterations (x read + x_new written) + the final
+    # build-only pass that reads x once (8*d bytes/step)
+    bytes_ = steps * (iters * alg["bytes"] + alg["bytes"] // 2)
+    flops = steps * iters * alg["flops"]
+    t = avg_ms * 1e-3
+    gbs = bytes_ / t / 1e9
+    tf = flops / t / 1e9  # GFLOP/s
+    ai = alg["flops"] / alg["bytes"]
+    ridge = fp64 / hbm
+    if ai > ridge:
+        return {"bound": "fp64", "achieved": round(tf, 1), "peak": fp64, "unit": "GFLOP/s",
+                "frac": round(tf / fp64, 4), "peak_source": fp64_src,
+                "hbm_achieved_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4),
+                "alg_bytes_per_launch": bytes_, "alg_flops_per_launch": flops, "traffic": None}
+    return {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(gbs / hbm, 4), "peak_source": hbm_src,
+            "fp64_achieved_gflops": round(tf, 1), "fp64_frac": round(tf / fp64, 4),
+            "alg_bytes_per_launch": bytes_, "alg_flops_per_launch": flops, "traffic": None}
+
+
+def cpu_baseline(cid: int, iters: int, seconds: float, n_override=None):
+    """The oracle (C restatement of the reference, all host cores) on a bounded sample."""
+    from oracle import oracle as O
+    from paper_2511_01465_b200.configs import CONFIGS
+    O.build_library()
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    cfg = CONFIGS[cid]
+    n = n_override or (cfg.oracle_n_steps or cfg.n_steps)
+    x0s = cfg.x0s()
+    pid = O.PROB[cfg.problem]
+    st = O.stepper_by_name(cfg.stepper)
+    b = 0
+    runs = 0
+    t0 = time.perf_counter()
+    while True:
+        x0 = x0s[b % x0s.shape[0]]
+        O.solve(pid, cfg.params, st, x0, np.tile(x0, (n, 1)), cfg.dt, iters,
+                abort_nonfinite=False)
+        runs += 1
+        b += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    val = runs * n * iters / el
+    sample = (f"{cfg.name}: {runs} oracle solve(s) of 1 trajectory x N={n} x {iters} fixed "
+              f"Newton iterations in {el:.1f} s")
+    return {"value": val, "unit": "Newton time-steps/s", "cores": cores, "kind": "port",
+            "sample": sample}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle port timed on the host cores, our config/metric."""
+    if rank != 0:
+        return
+    cid = cfg_id(args.workload)
+    from oracle import oracle as O
+    from paper_2511_01465_b200.configs import CONFIGS
+    O.build_library()
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    cfg = CONFIGS[cid]
+    n = cfg.oracle_n_steps or cfg.n_steps
+    if cid == 4:
+        n = 1024
+    x0 = cfg.x0s()[0]
+    pid = O.PROB[cfg.problem]
+    st = O.stepper_by_name(cfg.stepper)
+
+    def one():
+        O.solve(pid, cfg.params, st, x0, np.tile(x0, (n, 1)), cfg.dt, args.iters,
+                abort_nonfinite=False)
+    for _ in range(args.warmup):
+        one()
+    durs = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        one()
+        durs.append(time.perf_counter() - t0)
+    tot = sum(durs)
+    val = args.steps * n * args.iters / tot
+    sample = (f"{cfg.name}: per step one oracle solve of 1 trajectory x N={n} x {args.iters} "
+              f"fixed Newton iterations (C port of the reference, OpenMP {cores} threads)")
+    line = {
+        "metric": "Newton time-steps/s (Jacobian+scan)", "value": val,
+        "unit": "Newton time-steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": cfg.name, "n_steps": n, "batch": 1, "newton_iters": args.iters,
+                   "mode": "fixed iterations, non-aborting", "parallelism": "cpu"},
+        "cpu_baseline": {"value": val, "unit": "Newton time-steps/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "Newton time-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    hbm, hbm_src, fp64, fp64_src = peaks()
+    cid = cfg_id(args.workload)
+    w = Workload(cid, args.iters, rank=rank, world=world)
+    flush_buf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+
+    def flush():
+        flush_l2(flush_buf)
+
+    clocks = Clocks(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    durs, launches = time_steps(w, args.steps, args.warmup, flush)
+    clock_info = clocks.stop()
+    tot_ms = reduce_max(sum(durs), world)
+    units_per_step = w.B * w.n * args.iters * world
+    value = units_per_step * args.steps / (tot_ms * 1e-3)
+    avg_ms = tot_ms / args.steps
+    it, st, ix = w.outcome()
+
+    # e2e through the public API with host buffers
+    e2e_durs, h2d, d2h = e2e_steps(w, max(3, args.steps // 2), 2)
+    e2e_ms = reduce_max(sum(e2e_durs), world) / len(e2e_durs)
+    e2e_val = units_per_step / (e2e_ms * 1e-3)
+
+    # BASELINE stop-rule solve of the same config
+    w.set_mode(fixed=False)
+    sr_durs, _ = time_steps(w, 5, 2, flush)
+    sit, sst, six = w.outcome()
+    sr_ms = statistics.median(sr_durs)
+    names = {0: "MAXITER", 1: "CONVERGED", 2: "NONFINITE", 3: "SINGULAR"}
+    stop_rule = {"status": names.get(int(sst[0]), str(int(sst[0]))),
+                 "status_index": int(six[0]), "iterations": int(sit[0]), "solve_ms": sr_ms,
+                 "newton_steps_per_s": w.n * w.B * max(int(sit[0]), 1) / (sr_ms * 1e-3)}
+
+    roof = roofline_for(cid, w.n, w.B, args.iters, avg_ms, hbm, hbm_src, fp64, fp64_src)
+    prof_traffic = REPO / "profiles" / "traffic.json"
+    if prof_traffic.exists():
+        try:
+            tr = json.loads(prof_traffic.read_text()).get(args.workload)
+            if tr:
+                roof["traffic"] = tr
+        except ValueError:
+            pass
+
+    extra = {}
+    if not args.no_extra and world == 1:
+        for ocid in (1, 3, 5, 4):
+            try:
+                ow = Workload(ocid, args.iters)
+                od, _ = time_steps(ow, 5, 2, flush)
+                oms = statistics.median(od)
+                ov = ow.B * ow.n * args.iters / (oms * 1e-3)
+                ow.set_mode(fixed=False)
+                sd, _ = time_steps(ow, 3, 1, flush)
+                oi, os_, ox = ow.outcome()
+                extra[ow.cfg.name] = {
+                    "fixed_iters": args.iters, "ms": round(oms, 4), "newton_steps_per_s": ov,
+                    "roofline": roofline_for(ocid, ow.n, ow.B, args.iters, oms, hbm, hbm_src,
+                                             fp64, fp64_src),
+                    "stop_rule": {"ms": round(statistics.median(sd), 4),
+                                  "status_counts": {names.get(int(k), str(k)): int(v) for k, v in
+                                                    zip(*np.unique(os_, return_counts=True))},
+                                  "iterations_max": int(oi.max())},
+                }
+                del ow
+                torch.cuda.empty_cache()
+            except Exception as exc:  # report, never hide
+                extra[f"cfg{ocid}"] = {"error": f"{type(exc).__name__}: {exc}"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(cid, args.iters, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "Newton time-steps/s (Jacobian+scan)",
+            "value": value,
+            "unit": "Newton time-steps/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": avg_ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (BASELINE.json configs, seeded default_rng(0))",
+            "config": {"workload": w.cfg.name, "problem": w.cfg.problem, "stepper": w.cfg.stepper,
+                       "n_steps": w.n, "dim": w.d, "batch": w.B * world,
+                       "newton_iters": args.iters,
+                       "mode": "fixed iterations, non-aborting (SURVEY 8d)",
+                       "l2": "flushed between steps (256 MB write)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "Newton time-steps/s", "ms": e2e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clock_info,
+            "final_status": {"iters": int(it[0]), "status": int(st[0])},
+            "stop_rule": stop_rule,
+            "configs": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -106,6 +106,9 @@ int         odx_abi_version(void);
 const char* odx_last_error(void);
 /* 1 if (problem, stepper) has a compiled device path, else 0. */
 int         odx_supported(const odx_problem* P, const odx_stepper* S);
+/* Number of CUDA kernels this library has launched in this process (a
+ * monotone counter, used to report `gpu_launches` in bench.py).            */
+int64_t     odx_launch_count(void);
 
 /* ---- the solver ------------------------------------------------------------
  * Replaces odescan.solve()  newton_pint.py:326-406 (batched over B

@@ -27,7 +27,7 @@ PROB_LINEAR = 10
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "odx_abi_version", "odx_last_error", "odx_supported", "odx_solve_workspace_bytes",
+    "odx_abi_version", "odx_last_error", "odx_supported", "odx_launch_count", "odx_solve_workspace_bytes",
     "odx_solve", "odx_build_explicit", "odx_build_implicit",
     "odx_scan_affine_workspace_bytes", "odx_scan_affine", "odx_max_abs", "odx_add_inplace",
     "odx_shard_workspace_bytes", "odx_shard_local", "odx_shard_fixup",
@@ -73,6 +73,7 @@ def lib():
     P_, S_, CFG = C.POINTER(OdxProblem), C.POINTER(OdxStepper), C.POINTER(OdxNewtonCfg)
     L.odx_abi_version.restype = C.c_int
     L.odx_last_error.restype = C.c_char_p
+    L.odx_launch_count.restype = C.c_int64
     L.odx_supported.restype = C.c_int
     L.odx_supported.argtypes = [P_, S_]
     L.odx_solve_workspace_bytes.restype = sz

@@ -54,6 +54,7 @@ int build_op(const ProbParams& pp, const StepCoefs& sc, const double* x0, const 
                                                                                  ce, h, first_bad);
     if (KIND == 1) finalize_bad_kernel<<<1, 1, 0, st>>>(first_bad);
     ODX_CUDA(cudaGetLastError());
+    count_launch((N > 0 ? 1 : 0) + (KIND == 1 ? 2 : 0));
     return ODX_OK;
 }
 

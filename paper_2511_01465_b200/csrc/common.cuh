@@ -30,6 +30,7 @@ inline int fail(int code, const char* msg) {
     } while (0)
 
 int num_sms();
+void count_launch(int n = 1);
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 

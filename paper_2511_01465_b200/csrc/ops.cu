@@ -255,6 +255,7 @@ int scan_op_d(const double* F, const double* c, long long N, double* Fp, double*
     scan_op_kernel<D, SCAN_THREADS, SCAN_ITEMS><<<(unsigned)nt, SCAN_THREADS, 0, st>>>(
         F, c, N, Fp, cp, ctr, flags, aggbuf, inclbuf);
     ODX_CUDA(cudaGetLastError());
+    count_launch(1);
     return ODX_OK;
 }
 
@@ -306,6 +307,7 @@ int max_abs_op(const double* A, long long n, int d, double* out, cudaStream_t st
     max_abs_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, n, d,
                                                      reinterpret_cast<unsigned long long*>(out));
     ODX_CUDA(cudaGetLastError());
+    count_launch(1);
     return ODX_OK;
 }
 
@@ -322,6 +324,7 @@ int add_op(double* X, const double* U, long long n, int d, cudaStream_t st) {
     if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
     add_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, U, m);
     ODX_CUDA(cudaGetLastError());
+    count_launch(1);
     return ODX_OK;
 }
 

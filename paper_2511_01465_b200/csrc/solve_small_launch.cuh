@@ -2,9 +2,13 @@
 // kernels (resident and persistent).  Instantiated per problem by the generated
 // translation units under csrc/gen/ (see paper_2511_01465_b200/build.py).
 #pragma once
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "dispatch.cuh"
 #include "solve_small.cuh"
+#include "solve_ws.cuh"
 
 namespace odx {
 
@@ -18,6 +22,7 @@ int launch_resident(SolveParams& p, cudaStream_t st) {
     ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)p.B, THREADS, smem, st>>>(p);
     ODX_CUDA(cudaGetLastError());
+    count_launch(1);
     return ODX_OK;
 }
 
@@ -76,8 +81,80 @@ int launch_persistent(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st
     ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(THREADS),
                                          args, smem, st));
     ODX_CUDA(cudaGetLastError());
+    count_launch(2);  // init_bad_slots + the persistent solve
     return ODX_OK;
 }
+
+// Workspace of the warp-specialised solve: X ping-pong buffer, look-back
+// records (zeroed: tag 0 never matches an epoch), tile counters, reductions,
+// grid-barrier words.
+template <int D>
+struct WsLayout {
+    size_t total = 0, zero_off = 0, zero_bytes = 0;
+    size_t Xalt, recs, gsums, ctr, red, bar;
+    long long ntiles = 0;
+    WsLayout(long long N, long long T, int max_iters) {
+        ntiles = (N + T - 1) / T;
+        size_t off = 0;
+        auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
+        Xalt = at((size_t)N * D * sizeof(double));
+        zero_off = align_up(off, 256);
+        recs = at((size_t)ntiles * sizeof(LbRecord<D>));
+        gsums = at((size_t)((ntiles + 31) / 32 + 1) * (D * D + D) * sizeof(Chunk));
+        ctr = at(((size_t)max_iters + 1) * 4);
+        red = at(4 * ((size_t)max_iters + 1) * 8);
+        bar = at(2 * 4);
+        zero_bytes = off - zero_off;
+        total = off + 256;
+    }
+};
+
+template <class P, int KIND, int S, int NCW, int ITEMS>
+int launch_ws(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
+    using W = WsEngine<P, KIND, S, NCW, ITEMS>;
+    constexpr int D = P::D;
+    auto kern = persistent_ws_kernel<P, KIND, S, NCW, ITEMS>;
+    const WsLayout<D> lay(p.N, (long long)W::T, p.max_iters);
+    if (ws == nullptr || ws_bytes < lay.total)
+        return fail(ODX_EWORKSPACE, "workspace too small for persistent solve");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    WsParams wp;
+    wp.sp = p;
+    wp.sp.Xalt = reinterpret_cast<double*>(base + lay.Xalt);
+    wp.sp.ctr = reinterpret_cast<uint32_t*>(base + lay.ctr);
+    wp.sp.red = reinterpret_cast<unsigned long long*>(base + lay.red);
+    wp.sp.bar = reinterpret_cast<unsigned*>(base + lay.bar);
+    wp.sp.ntiles = lay.ntiles;
+    wp.recs = base + lay.recs;
+    wp.gsums = base + lay.gsums;
+    ODX_CUDA(cudaMemsetAsync(base + lay.zero_off, 0, lay.zero_bytes, st));
+    init_bad_slots(wp.sp.red, p.max_iters + 1, st);
+    const size_t smem = sizeof(typename W::Shared);
+    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::NT, smem));
+    if (per_sm < 1) return fail(ODX_ECUDA, "persistent kernel cannot be resident");
+    long long grid = (long long)per_sm * num_sms();
+    if (grid > lay.ntiles) grid = lay.ntiles;
+    void* args[] = {&wp};
+    ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(W::NT), args,
+                                         smem, st));
+    ODX_CUDA(cudaGetLastError());
+    count_launch(2);  // init_bad_slots + the persistent solve
+    return ODX_OK;
+}
+
+inline bool use_legacy_persistent() {
+    static const bool legacy = [] {
+        const char* v = std::getenv("ODX_PERSISTENT");
+        return v && std::strcmp(v, "legacy") == 0;
+    }();
+    return legacy;
+}
+
+// items per compute thread of the warp-specialised kernel, by state dim
+template <int D>
+constexpr int ws_items() { return D == 1 ? 8 : (D == 2 ? 4 : 2); }
 
 }  // namespace
 
@@ -89,11 +166,18 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
     constexpr int RI = (D <= 3) ? 8 : 4;   // items per thread, resident
     constexpr int PI = (D <= 2) ? 4 : 2;   // items per thread, persistent
     const bool resident = p.N <= 256LL * RI;
+    constexpr int WI = ws_items<D>();
+    const bool small_ws = p.N < 128LL * WI * 296;  // keep >= 2 tiles per SM
     if (query) {
         *need = 0;
         if (!resident) {
-            const long long T = (p.N < 128LL * PI * 296) ? 128 : 128LL * PI;
-            *need = PersistLayout<D>(p.N, T, p.max_iters).total;
+            if (use_legacy_persistent()) {
+                const long long T = (p.N < 128LL * PI * 296) ? 128 : 128LL * PI;
+                *need = PersistLayout<D>(p.N, T, p.max_iters).total;
+            } else {
+                const long long T = small_ws ? 128 : 128LL * WI;
+                *need = WsLayout<D>(p.N, T, p.max_iters).total;
+            }
         }
         return ODX_OK;
     }
@@ -102,9 +186,13 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
         return launch_resident<P, KIND, S, 256, RI>(p, st);
     }
     if (p.B != 1) return fail(ODX_EUNSUPPORTED, "batched solve needs N <= resident limit");
-    // small N: 1 item/thread keeps >= 2 tiles per SM; large N: PI items/thread
-    if (p.N < 128LL * PI * 296) return launch_persistent<P, KIND, S, 128, 1>(p, ws, ws_bytes, st);
-    return launch_persistent<P, KIND, S, 128, PI>(p, ws, ws_bytes, st);
+    if (use_legacy_persistent()) {
+        // small N: 1 item/thread keeps >= 2 tiles per SM; large N: PI items/thread
+        if (p.N < 128LL * PI * 296) return launch_persistent<P, KIND, S, 128, 1>(p, ws, ws_bytes, st);
+        return launch_persistent<P, KIND, S, 128, PI>(p, ws, ws_bytes, st);
+    }
+    if (small_ws) return launch_ws<P, KIND, S, 4, 1>(p, ws, ws_bytes, st);
+    return launch_ws<P, KIND, S, 4, WI>(p, ws, ws_bytes, st);
 }
 
 }  // namespace odx

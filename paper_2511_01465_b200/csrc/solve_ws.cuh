@@ -1,0 +1,672 @@
+// solve_ws.cuh — warp-specialised persistent Newton solve for long trajectories.
+//
+// Per CTA: NCW compute warps (CW) + 1 control warp (CTL).  Tiles of
+// T = NCW*32*ITEMS consecutive steps are claimed in order from a per-iteration
+// counter and flow through a two-buffer pipeline:
+//
+//   CTL: [wait AGG_b] decoupled look-back for the tile whose aggregate CW
+//        just published, publish its inclusive prefix, hand the tile's
+//        incoming state to CW [arrive PREF_b] -> only then claim the tile
+//        after next and TMA-copy its rows into staging buffer b (mbarrier),
+//        so no tile is ever claimed by a CTA that is blocked on a look-back
+//   CW:  [wait mbarrier] build the tile's elements (residual + step-map
+//        Jacobian, _kernels.py:299-342 / :393-464) in registers, keep its X
+//        rows in registers, fold, warp scan, park elements in smem
+//        [arrive AGG_b] -> apply the PREVIOUS tile's prefix [wait PREF_b']
+//        -> X + dx into an output staging buffer -> TMA bulk store
+//
+// so the look-back of tile i (CTL) overlaps the build of tile i+1 (CW), and
+// the HBM loads of tile i+2 overlap both.  Look-back records are
+// self-validating 16-byte {value, tag} chunks (sm100.cuh): one L2 round trip
+// per 32-tile window, no flag/fence handshake.  One grid barrier per Newton
+// iteration; every CTA takes the same on-device decision afterwards
+// (newton_pint.py:373-394 + the BASELINE step rule).
+#pragma once
+
+#include "sm100.cuh"
+#include "solve_small.cuh"
+
+namespace odx {
+
+enum : uint32_t { BAR_AGG = 1, BAR_PREF = 3, BAR_CW = 5 };
+
+// Optional pipeline trace (build with -DODX_TRACE): per tile of Newton
+// iteration ODX_TRACE_IT, 8 %globaltimer stamps:
+//   0 CW build start  1 CW aggregate published  2 CTL look-back start
+//   3 CTL look-back end  4 CW apply start (prefix received)  5 CW apply end
+//   6 CTL claim  7 CTA id
+#ifdef ODX_TRACE
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(it_, t_, k_, v_)                                              \
+    do {                                                                    \
+        if (g_trace && (it_) == 1) g_trace[(t_) * 8 + (k_)] = (v_);         \
+    } while (0)
+#else
+#define TRACE(it_, t_, k_, v_) do { } while (0)
+__device__ __forceinline__ unsigned long long gtime() { return 0; }
+#endif
+
+template <int D>
+struct LbRecord {
+    Chunk agg[D * D + D];
+    Chunk incl[D];
+};
+
+struct WsParams {
+    SolveParams sp;
+    void* recs;   // LbRecord<D>[ntiles]
+    void* gsums;  // Chunk[nblocks32][D*D+D]: aggregates of aligned 32-tile blocks
+};
+
+// Poll one look-back record until it is usable in this epoch.  want_agg:
+// also require the AGG payload (block-boundary tiles need every aggregate).
+// Returns 2 if the inclusive prefix is valid (e = (0, prefix)), else 1 with
+// e = the tile aggregate.
+template <int D>
+__device__ __forceinline__ int lb_poll(const LbRecord<D>* rec, unsigned long long tagA,
+                                       unsigned long long tagI, bool want_agg, Elem<D>& e,
+                                       Elem<D>& aggv) {
+    // Poll only the first chunk of each payload (cheap on L2); fetch the rest
+    // once a tag matches and re-verify every chunk (self-validating records).
+    unsigned sleep_ns = 32;  // spin count (short sleeps after a few polls)
+    while (true) {
+        const Chunk i0 = ld_chunk(&rec->incl[0]);
+        const Chunk a0 = ld_chunk(&rec->agg[0]);
+        const bool iv0 = (i0.tag == tagI), av0 = (a0.tag == tagA);
+        if (av0 || (iv0 && !want_agg)) {
+            bool iv = iv0, av = av0;
+            double ci[D];
+            ci[0] = i0.v;
+#pragma unroll
+            for (int k = 1; k < D; k++) {
+                Chunk ch = ld_chunk(&rec->incl[k]);
+                ci[k] = ch.v;
+                iv &= (ch.tag == tagI);
+            }
+            if (av0) {
+                aggv.F[0] = a0.v;
+#pragma unroll
+                for (int k = 1; k < D * D; k++) {
+                    Chunk ch = ld_chunk(&rec->agg[k]);
+                    aggv.F[k] = ch.v;
+                    av &= (ch.tag == tagA);
+                }
+#pragma unroll
+                for (int k = 0; k < D; k++) {
+                    Chunk ch = ld_chunk(&rec->agg[D * D + k]);
+                    aggv.c[k] = ch.v;
+                    av &= (ch.tag == tagA);
+                }
+            }
+            if (iv && (av || !want_agg)) {
+#pragma unroll
+                for (int k = 0; k < D * D; k++) e.F[k] = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; k++) e.c[k] = ci[k];
+                return 2;
+            }
+            if (av) {
+                e = aggv;
+                return 1;
+            }
+        }
+        if (++sleep_ns > 40) __nanosleep(16);
+    }
+}
+
+// Two-level decoupled look-back for tile t (all 32 lanes of the control warp).
+// Level 1 walks tile records (32 tiles per round); once past the most recent
+// 32 tiles it aligns to 32-tile blocks and walks block aggregates (1024 tiles
+// per round).  The first tile of every block publishes the previous block's
+// aggregate, so the inclusive-prefix frontier is never more than a couple of
+// rounds away.  Returns the exclusive prefix state in z (lane 0).
+template <int D, bool LEVEL2>
+__device__ __forceinline__ void lookback2(long long t, unsigned long long tagA,
+                                          unsigned long long tagI, unsigned long long tagG,
+                                          LbRecord<D>* recs, Chunk* gsums, double* z, int lane) {
+    constexpr int E = D * D + D;
+    Elem<D> R;
+    bool R_has = false;
+    auto fold = [&](Elem<D>& e, bool has) {
+        warp_reduce_latest_first<D>(e, has, lane);
+        if (lane == 0 && has) {
+            if (R_has)
+                compose<D>(e, R, R);
+            else {
+                R = e;
+                R_has = true;
+            }
+        }
+    };
+    auto sentinel = [&](Elem<D>& e) {  // the state before tile 0 is the zero offset
+#pragma unroll
+        for (int k = 0; k < D * D; k++) e.F[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; k++) e.c[k] = 0.0;
+    };
+    // ---- round 1: tiles t-1 .. t-32 --------------------------------------
+    const bool block_start = LEVEL2 && (t % 32 == 0);
+    {
+        const long long j = t - 1 - lane;
+        Elem<D> e, av;
+        int kind = 2;
+        if (j >= 0)
+            kind = lb_poll<D>(&recs[j], tagA, tagI, block_start, e, av);
+        else
+            sentinel(e);
+        if (block_start) {
+            // publish the aggregate of block t/32 - 1 (tiles t-32 .. t-1)
+            Elem<D> g = av;
+            bool gh = true;
+            warp_reduce_latest_first<D>(g, gh, lane);
+            if (lane == 0) {
+                Chunk* dst = gsums + (t / 32 - 1) * E;
+#pragma unroll
+                for (int k = 0; k < D * D; k++) st_chunk(dst + k, g.F[k], tagG);
+#pragma unroll
+                for (int k = 0; k < D; k++) st_chunk(dst + D * D + k, g.c[k], tagG);
+            }
+        }
+        const unsigned m = __ballot_sync(FULL, kind == 2);
+        const int first = m ? (__ffs(m) - 1) : 32;
+        fold(e, lane <= first);
+        if (first < 32) goto done;
+    }
+    if (!LEVEL2) {
+        // plain decoupled look-back: 32 tiles per round
+        long long pos = t - 33;
+        while (true) {
+            const long long j = pos - lane;
+            Elem<D> e, av;
+            int kind = 2;
+            if (j >= 0)
+                kind = lb_poll<D>(&recs[j], tagA, tagI, false, e, av);
+            else
+                sentinel(e);
+            const unsigned m = __ballot_sync(FULL, kind == 2);
+            const int first = m ? (__ffs(m) - 1) : 32;
+            fold(e, lane <= first);
+            if (first < 32) goto done;
+            pos -= 32;
+        }
+    }
+    {
+        long long q = t - 33;  // newest tile not yet folded (q >= 0 here)
+        // ---- partial round up to the block boundary -----------------------
+        if ((q & 31) != 31) {
+            const int n = (int)(q & 31) + 1;
+            const long long j = q - lane;
+            Elem<D> e, av;
+            int kind = 2;
+            if (lane < n)
+                kind = lb_poll<D>(&recs[j], tagA, tagI, false, e, av);
+            else
+                sentinel(e);
+            const unsigned m = __ballot_sync(FULL, kind == 2 && lane < n);
+            const int first = m ? (__ffs(m) - 1) : 32;
+            fold(e, lane <= first && lane < n);
+            if (first < 32) goto done;
+            q -= n;
+        }
+        // ---- level 2: whole blocks ending at q (q = 32k + 31) -------------
+        while (true) {
+            const long long kb = (q + 1) / 32 - 1 - lane;  // block of this lane
+            Elem<D> e;
+            int kind = 2;
+            if (kb >= 0) {
+                const long long last = kb * 32 + 31;
+                const Chunk* g = gsums + kb * E;
+                int spins = 0;
+                while (true) {
+                    bool iv = true, gv = true;
+                    double ci[D];
+#pragma unroll
+                    for (int k = 0; k < D; k++) {
+                        Chunk ch = ld_chunk(&recs[last].incl[k]);
+                        ci[k] = ch.v;
+                        iv &= (ch.tag == tagI);
+                    }
+                    if (iv) {
+#pragma unroll
+                        for (int k = 0; k < D * D; k++) e.F[k] = 0.0;
+#pragma unroll
+                        for (int k = 0; k < D; k++) e.c[k] = ci[k];
+                        kind = 2;
+                        break;
+                    }
+#pragma unroll
+                    for (int k = 0; k < E; k++) {
+                        Chunk ch = ld_chunk(g + k);
+                        if (k < D * D)
+                            e.F[k] = ch.v;
+                        else
+                            e.c[k - D * D] = ch.v;
+                        gv &= (ch.tag == tagG);
+                    }
+                    if (gv) {
+                        kind = 1;
+                        break;
+                    }
+                    if (++spins > 4) __nanosleep(20);
+                }
+            } else {
+                sentinel(e);
+            }
+            const unsigned m = __ballot_sync(FULL, kind == 2);
+            const int first = m ? (__ffs(m) - 1) : 32;
+            fold(e, lane <= first);
+            if (first < 32) break;
+            q -= 32 * 32;
+        }
+    }
+done:
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < D; k++) z[k] = R.c[k];
+    }
+}
+
+template <class P, int KIND, int S, int NCW, int ITEMS>
+struct WsEngine {
+    static constexpr int D = P::D;
+    static constexpr int E = D * D + D;
+    static constexpr int NCT = NCW * 32;
+    static constexpr int NT = NCT + 32;
+    static constexpr int T = NCT * ITEMS;
+    static constexpr int EST = ITEMS * E + (((ITEMS * E) & 1) ? 0 : 1);  // odd stride
+    static constexpr int AGS = E + ((E & 1) ? 0 : 1);
+
+    struct Shared {
+        double xr[2][T * D];  // tile rows; first member => 16-byte aligned TMA target
+        double xo[2][T * D];  // X + dx staging for the TMA bulk store
+        double xh[2][D];      // halo: the state before the tile's first step
+        double els[2][NCT * EST];
+        double tin[2][NCT * AGS];
+        double wt[2][NCW][E];
+        int thas[2][NCT];
+        int wthas[2][NCW];
+        double z[2][D];
+        double A[2][D * D + D];  // tile aggregate (composed and published by CW thread 0)
+        long long tile[2];
+        uint64_t mbar[2];
+        double redd[3][NCW];
+        unsigned long long redb[NCW];
+    };
+};
+
+__device__ __forceinline__ unsigned long long lb_tag(uint32_t epoch, uint32_t kind) {
+    return ((unsigned long long)epoch << 2) | kind;
+}
+
+template <class P, int KIND, int S, int NCW, int ITEMS>
+__global__ void __launch_bounds__((NCW + 1) * 32, 2)
+persistent_ws_kernel(const WsParams wp) {
+    using W = WsEngine<P, KIND, S, NCW, ITEMS>;
+    constexpr int D = W::D, E = W::E, NCT = W::NCT, NT = W::NT, T = W::T;
+    constexpr int EST = W::EST, AGS = W::AGS;
+    using Rec = LbRecord<D>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typename W::Shared& sm = *reinterpret_cast<typename W::Shared*>(smem_raw);
+
+    const SolveParams& p = wp.sp;
+    Rec* recs = reinterpret_cast<Rec*>(wp.recs);
+    Chunk* gsums = reinterpret_cast<Chunk*>(wp.gsums);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const bool is_ctl = (w == NCW);
+    const long long N = p.N;
+    const unsigned nblocks = gridDim.x;
+
+    if (tid == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    double* cur = p.X;
+    double* nxt = p.Xalt;
+    double step_prev = __longlong_as_double(0x7ff8000000000000ll);
+    Decision dd{0, -1, -1, 0};
+    uint32_t ph0 = 0, ph1 = 0;  // CW: mbarrier phase parity per buffer
+
+    for (int it = 0; it <= p.max_iters; it++) {
+        const bool do_scan = it < p.max_iters;
+        const uint32_t epoch = (uint32_t)it + 1u;
+        const unsigned long long tagA = lb_tag(epoch, 1), tagI = lb_tag(epoch, 2);
+        const unsigned long long tagG = lb_tag(epoch, 3);
+
+        if (is_ctl) {
+            // ------------------------------------------------ control warp --
+            fence_proxy_async_global();
+            auto claim = [&]() -> long long {
+                long long t = 0;
+                if (lane == 0) t = (long long)atomicAdd(p.ctr + it, 1u);
+                t = __shfl_sync(FULL, t, 0);
+                if (lane == 0 && t < p.ntiles) {
+                    TRACE(it, t, 6, gtime());
+                    TRACE(it, t, 7, (unsigned long long)blockIdx.x);
+                }
+                return t < p.ntiles ? t : -1;
+            };
+            auto issue = [&](int b, long long t) {
+                if (lane == 0) {
+                    sm.tile[b] = t;
+                    if (t >= 0) {
+                        const long long base = t * T;
+                        const long long rows = (N - base) < T ? (N - base) : T;
+                        for (int j = 0; j < D; j++)
+                            sm.xh[b][j] = (base == 0) ? p.x0[j] : __ldcg(cur + (base - 1) * D + j);
+                        uint32_t bytes = (uint32_t)(rows * D * 8);
+                        uint32_t tma_bytes = bytes & ~15u;
+                        for (uint32_t q = tma_bytes / 8; q < bytes / 8; q++)
+                            sm.xr[b][q] = __ldcg(cur + base * D + q);
+                        if (tma_bytes) {
+                            mbar_arrive_expect_tx(&sm.mbar[b], tma_bytes);
+                            tma_load_1d(sm.xr[b], cur + base * D, tma_bytes, &sm.mbar[b]);
+                        } else {
+                            mbar_arrive(&sm.mbar[b]);
+                        }
+                    } else {
+                        mbar_arrive(&sm.mbar[b]);
+                    }
+                }
+                __syncwarp();
+            };
+            long long mt[2];
+            mt[0] = claim();
+            issue(0, mt[0]);
+            mt[1] = -1;
+            if (mt[0] >= 0) {
+                mt[1] = claim();
+                issue(1, mt[1]);
+            }
+            for (int i = 0;; i++) {
+                const int b = i & 1;
+                const long long t = mt[b];
+                if (t < 0) break;
+                named_sync2<BAR_AGG, NT>(b);
+                if (lane == 0) TRACE(it, t, 2, gtime());
+                if (do_scan) {
+                    // the tile aggregate was composed and published by CW thread 0
+                    Elem<D> A;
+#pragma unroll
+                    for (int k = 0; k < D * D; k++) A.F[k] = sm.A[b][k];
+#pragma unroll
+                    for (int k = 0; k < D; k++) A.c[k] = sm.A[b][D * D + k];
+                    double z[D];
+#pragma unroll
+                    for (int k = 0; k < D; k++) z[k] = 0.0;
+                    if (t > 0) lookback2<D, false>(t, tagA, tagI, tagG, recs, gsums, z, lane);
+                    if (lane == 0) {
+                        double incl[D];
+                        apply<D>(A, z, incl);
+#pragma unroll
+                        for (int k = 0; k < D; k++) st_chunk(&recs[t].incl[k], incl[k], tagI);
+#pragma unroll
+                        for (int k = 0; k < D; k++) sm.z[b][k] = z[k];
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) TRACE(it, t, 3, gtime());
+                named_arrive2<BAR_PREF, NT>(b);
+                // Claim the tile after next only now: the compute warps will
+                // build it right after applying this tile, so a claimed tile
+                // never waits behind a look-back (no convoys).  Its rows land
+                // in staging buffer b (consumed by this tile's build) while
+                // the compute warps apply this tile.
+                long long tn = -1;
+                if (mt[b ^ 1] >= 0) {
+                    tn = claim();
+                    issue(b, tn);
+                }
+                mt[b] = tn;
+            }
+        } else {
+            // ------------------------------------------------ compute warps --
+            double rn = 0.0, scn = 0.0, step = 0.0;
+            unsigned long long bad = ~0ull;
+            const P prob(p.prob);
+            auto row = [&](int b, int r, int j) -> double {
+                return r < 0 ? sm.xh[b][j] : sm.xr[b][r * D + j];
+            };
+            // apply tile (buffer c, first step `base`, its X rows in xk)
+            auto apply_tile = [&](int c, long long base, const double (&xk)[ITEMS][D]) {
+                named_sync2<BAR_PREF, NT>(c);
+                if (tid == 0) TRACE(it, base / T, 4, gtime());
+                if (!do_scan) return;
+                double z[D];
+#pragma unroll
+                for (int k = 0; k < D; k++) z[k] = sm.z[c][k];
+                for (int q = 0; q < w; q++) {
+                    if (!sm.wthas[c][q]) continue;
+                    Elem<D> e;
+#pragma unroll
+                    for (int k = 0; k < D * D; k++) e.F[k] = sm.wt[c][q][k];
+#pragma unroll
+                    for (int k = 0; k < D; k++) e.c[k] = sm.wt[c][q][D * D + k];
+                    apply<D>(e, z, z);
+                }
+                if (lane > 0 && sm.thas[c][tid - 1]) {
+                    Elem<D> e;
+                    const double* src = &sm.tin[c][(tid - 1) * AGS];
+#pragma unroll
+                    for (int k = 0; k < D * D; k++) e.F[k] = src[k];
+#pragma unroll
+                    for (int k = 0; k < D; k++) e.c[k] = src[D * D + k];
+                    apply<D>(e, z, z);
+                }
+#pragma unroll
+                for (int i = 0; i < ITEMS; i++) {
+                    const int r = tid * ITEMS + i;
+                    if (base + r < N) {
+                        Elem<D> e;
+                        const double* src = &sm.els[c][tid * EST + i * E];
+#pragma unroll
+                        for (int k = 0; k < D * D; k++) e.F[k] = src[k];
+#pragma unroll
+                        for (int k = 0; k < D; k++) e.c[k] = src[D * D + k];
+                        double dx[D];
+                        apply<D>(e, z, dx);
+                        step = nan_drop_max(step, row_max_abs<D>(dx));
+#pragma unroll
+                        for (int k = 0; k < D; k++) {
+                            z[k] = dx[k];
+                            sm.xo[c][r * D + k] = xk[i][k] + dx[k];
+                        }
+                    }
+                }
+                named_sync<BAR_CW, NCT>();
+                const long long rows = (N - base) < T ? (N - base) : T;
+                const uint32_t bytes = (uint32_t)(rows * D * 8);
+                if ((bytes & 15u) == 0) {
+                    if (tid == 0) {
+                        fence_proxy_async_smem();
+                        tma_store_1d(nxt + base * D, sm.xo[c], bytes);
+                        tma_store_commit();
+                        // the other staging buffer's store must have been read
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    }
+                } else {
+                    for (int q = tid; q < rows * D; q += NCT) nxt[base * D + q] = sm.xo[c][q];
+                }
+                if (tid == 0) TRACE(it, base / T, 5, gtime());
+            };
+            double xkp[ITEMS][D];
+            long long basep = 0;
+            int i = 0;
+            for (;; i++) {
+                const int b = i & 1;
+                if (b == 0) {
+                    mbar_wait(&sm.mbar[0], ph0);
+                    ph0 ^= 1u;
+                } else {
+                    mbar_wait(&sm.mbar[1], ph1);
+                    ph1 ^= 1u;
+                }
+                const long long t = sm.tile[b];
+                if (t < 0) break;
+                if (tid == 0) TRACE(it, t, 0, gtime());
+                const long long base = t * T;
+                Elem<D> el[ITEMS];
+                double xkc[ITEMS][D];
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++) {
+                    const int r = tid * ITEMS + q;
+                    const long long k = base + r;
+                    if (k < N) {
+                        double prev[D], h[D];
+#pragma unroll
+                        for (int j = 0; j < D; j++) {
+                            prev[j] = row(b, r - 1, j);
+                            xkc[q][j] = row(b, r, j);
+                        }
+                        bool sing = build_step<P, KIND, S>(prob, p.sc, prev, xkc[q], k == 0, el[q], h);
+                        rn = nan_drop_max(rn, row_max_abs<D>(h));
+                        if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(el[q].c));
+                        if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
+                    }
+                }
+                if (do_scan) {
+                    Elem<D> agg;
+                    bool has = false;
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++) {
+                        if (base + tid * ITEMS + q < N) {
+                            double* dst = &sm.els[b][tid * EST + q * E];
+#pragma unroll
+                            for (int k = 0; k < D * D; k++) dst[k] = el[q].F[k];
+#pragma unroll
+                            for (int k = 0; k < D; k++) dst[D * D + k] = el[q].c[k];
+                            if (has)
+                                compose<D>(agg, el[q], agg);
+                            else {
+                                agg = el[q];
+                                has = true;
+                            }
+                        }
+                    }
+                    if (!has) set_identity<D>(agg);
+                    warp_inclusive_scan<D>(agg, has, lane);
+                    double* dst = &sm.tin[b][tid * AGS];
+#pragma unroll
+                    for (int k = 0; k < D * D; k++) dst[k] = agg.F[k];
+#pragma unroll
+                    for (int k = 0; k < D; k++) dst[D * D + k] = agg.c[k];
+                    sm.thas[b][tid] = has ? 1 : 0;
+                    if (lane == 31) {
+#pragma unroll
+                        for (int k = 0; k < D * D; k++) sm.wt[b][w][k] = agg.F[k];
+#pragma unroll
+                        for (int k = 0; k < D; k++) sm.wt[b][w][D * D + k] = agg.c[k];
+                        sm.wthas[b][w] = has ? 1 : 0;
+                    }
+                    // publish this tile's aggregate now, not when the control
+                    // warp gets to it: look-backs must never queue behind
+                    // another tile's look-back
+                    named_sync<BAR_CW, NCT>();
+                    if (tid == 0) {
+                        Elem<D> A;
+                        bool A_has = false;
+                        for (int q = 0; q < NCW; q++) {
+                            if (!sm.wthas[b][q]) continue;
+                            Elem<D> e;
+#pragma unroll
+                            for (int k = 0; k < D * D; k++) e.F[k] = sm.wt[b][q][k];
+#pragma unroll
+                            for (int k = 0; k < D; k++) e.c[k] = sm.wt[b][q][D * D + k];
+                            if (A_has)
+                                compose<D>(A, e, A);
+                            else {
+                                A = e;
+                                A_has = true;
+                            }
+                        }
+                        if (!A_has) set_identity<D>(A);
+#pragma unroll
+                        for (int k = 0; k < D * D; k++) st_chunk(&recs[t].agg[k], A.F[k], tagA);
+#pragma unroll
+                        for (int k = 0; k < D; k++) st_chunk(&recs[t].agg[D * D + k], A.c[k], tagA);
+                        TRACE(it, t, 1, gtime());
+#pragma unroll
+                        for (int k = 0; k < D * D; k++) sm.A[b][k] = A.F[k];
+#pragma unroll
+                        for (int k = 0; k < D; k++) sm.A[b][D * D + k] = A.c[k];
+                    }
+                }
+                named_arrive2<BAR_AGG, NT>(b);
+                if (i > 0) apply_tile(b ^ 1, basep, xkp);
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++)
+#pragma unroll
+                    for (int j = 0; j < D; j++) xkp[q][j] = xkc[q][j];
+                basep = base;
+            }
+            if (i > 0) apply_tile((i - 1) & 1, basep, xkp);
+            if (tid == 0) {
+                tma_store_wait_all();
+                fence_proxy_async_global();
+            }
+            // block reduction over the compute warps -> one atomic each
+            rn = warp_max_nan_drop(rn);
+            scn = warp_max_nan_drop(scn);
+            step = warp_max_nan_drop(step);
+            bad = warp_min_u64(bad);
+            if (lane == 0) {
+                sm.redd[0][w] = rn;
+                sm.redd[1][w] = scn;
+                sm.redd[2][w] = step;
+                sm.redb[w] = bad;
+            }
+            named_sync<BAR_CW, NCT>();
+            if (tid == 0) {
+                double a = 0.0, c = 0.0, s = 0.0;
+                unsigned long long m = ~0ull;
+                for (int q = 0; q < NCW; q++) {
+                    a = fmax(a, sm.redd[0][q]);
+                    c = fmax(c, sm.redd[1][q]);
+                    s = fmax(s, sm.redd[2][q]);
+                    m = sm.redb[q] < m ? sm.redb[q] : m;
+                }
+                unsigned long long* red = p.red + 4ll * it;
+                if (a > 0.0) atomicMax(red + 0, dbits(a));
+                if (c > 0.0) atomicMax(red + 1, dbits(c));
+                if (s > 0.0) atomicMax(red + 2, dbits(s));
+                if (m != ~0ull) atomicMin(red + 3, m);
+            }
+        }
+        grid_barrier(p.bar, p.bar + 1, nblocks);
+        if (tid == 0) (void)ld_acquire_gpu_u32(p.bar + 1);
+        __syncthreads();
+        const unsigned long long* red = p.red + 4ll * it;
+        const double rnb = bitsd(__ldcg(red + 0));
+        const double scb = (KIND == 0) ? rnb : bitsd(__ldcg(red + 1));
+        const unsigned long long badb = __ldcg(red + 3);
+        dd = decide(it, p, rnb, badb, step_prev);
+        if (blockIdx.x == 0 && tid == 0 && dd.status != ODX_ST_SINGULAR) {
+            if (p.hist) p.hist[it] = rnb;
+            if (p.shist) p.shist[it] = scb;
+        }
+        if (dd.stop) break;
+        step_prev = bitsd(__ldcg(red + 2));
+        double* t2 = cur;
+        cur = nxt;
+        nxt = t2;
+    }
+    if (cur != p.X) {
+        const long long total = N * D;
+        for (long long q = (long long)blockIdx.x * NT + tid; q < total; q += (long long)nblocks * NT)
+            p.X[q] = __ldcg(cur + q);
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        p.iters[0] = dd.iters;
+        p.status[0] = dd.status;
+        p.sidx[0] = dd.index;
+    }
+}
+
+}  // namespace odx
