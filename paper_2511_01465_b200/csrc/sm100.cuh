@@ -90,7 +90,7 @@ __device__ __forceinline__ void named_arrive2(int b) {
 // A look-back payload chunk is {value, tag}: written and read as one aligned
 // 16-byte access, so a reader either sees the tag of the current epoch
 // together with its value, or an old tag — no flag/fence round trip needed.
-struct Chunk {
+struct alignas(16) Chunk {
     double v;
     unsigned long long tag;
 };

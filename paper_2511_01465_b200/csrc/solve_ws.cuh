@@ -44,7 +44,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #define TRACE(it_, t_, k_, v_)                                              \
     do {                                                                    \
-        if (g_trace && (it_) == 1) g_trace[(t_) * 8 + (k_)] = (v_);         \
+        if (g_trace && (it_) == 1) g_trace[(t_) * 16 + (k_)] = (v_);        \
     } while (0)
 #else
 #define TRACE(it_, t_, k_, v_) do { } while (0)
@@ -292,6 +292,8 @@ struct WsEngine {
         int wthas[2][NCW];
         double z[2][D];
         double A[2][D * D + D];  // tile aggregate (composed and published by CW thread 0)
+        double wex[2][NCW][D * D + D];  // exclusive composition of warp totals 0..w-1
+        int wexhas[2][NCW];
         long long tile[2];
         uint64_t mbar[2];
         double redd[3][NCW];
@@ -322,8 +324,8 @@ persistent_ws_kernel(const WsParams wp) {
     const unsigned nblocks = gridDim.x;
 
     if (tid == 0) {
-        mbar_init(&sm.mbar[0], 1);
-        mbar_init(&sm.mbar[1], 1);
+        mbar_init(&sm.mbar[0], 2);  // TMA (expect_tx) + cp.async halo arrival
+        mbar_init(&sm.mbar[1], 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -353,18 +355,31 @@ persistent_ws_kernel(const WsParams wp) {
                 }
                 return t < p.ntiles ? t : -1;
             };
+            // stage tile t into slot b: rows via TMA (expect_tx), the halo row
+            // via cp.async (arrives on the same mbarrier when it lands), so the
+            // control warp never blocks on a global load here
             auto issue = [&](int b, long long t) {
                 if (lane == 0) {
                     sm.tile[b] = t;
                     if (t >= 0) {
                         const long long base = t * T;
                         const long long rows = (N - base) < T ? (N - base) : T;
-                        for (int j = 0; j < D; j++)
-                            sm.xh[b][j] = (base == 0) ? p.x0[j] : __ldcg(cur + (base - 1) * D + j);
+                        if (base == 0) {
+                            for (int q = 0; q < D; q++) sm.xh[b][q] = p.x0[q];
+                        } else {
+                            for (int q = 0; q < D; q++)
+                                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                                                 smem_u32(&sm.xh[b][q])),
+                                             "l"(cur + (base - 1) * D + q)
+                                             : "memory");
+                        }
                         uint32_t bytes = (uint32_t)(rows * D * 8);
                         uint32_t tma_bytes = bytes & ~15u;
                         for (uint32_t q = tma_bytes / 8; q < bytes / 8; q++)
                             sm.xr[b][q] = __ldcg(cur + base * D + q);
+                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                                         smem_u32(&sm.mbar[b]))
+                                     : "memory");
                         if (tma_bytes) {
                             mbar_arrive_expect_tx(&sm.mbar[b], tma_bytes);
                             tma_load_1d(sm.xr[b], cur + base * D, tma_bytes, &sm.mbar[b]);
@@ -372,6 +387,7 @@ persistent_ws_kernel(const WsParams wp) {
                             mbar_arrive(&sm.mbar[b]);
                         }
                     } else {
+                        mbar_arrive(&sm.mbar[b]);
                         mbar_arrive(&sm.mbar[b]);
                     }
                 }
@@ -442,13 +458,12 @@ persistent_ws_kernel(const WsParams wp) {
                 double z[D];
 #pragma unroll
                 for (int k = 0; k < D; k++) z[k] = sm.z[c][k];
-                for (int q = 0; q < w; q++) {
-                    if (!sm.wthas[c][q]) continue;
+                if (sm.wexhas[c][w]) {
                     Elem<D> e;
 #pragma unroll
-                    for (int k = 0; k < D * D; k++) e.F[k] = sm.wt[c][q][k];
+                    for (int k = 0; k < D * D; k++) e.F[k] = sm.wex[c][w][k];
 #pragma unroll
-                    for (int k = 0; k < D; k++) e.c[k] = sm.wt[c][q][D * D + k];
+                    for (int k = 0; k < D; k++) e.c[k] = sm.wex[c][w][D * D + k];
                     apply<D>(e, z, z);
                 }
                 if (lane > 0 && sm.thas[c][tid - 1]) {
@@ -573,6 +588,13 @@ persistent_ws_kernel(const WsParams wp) {
                         Elem<D> A;
                         bool A_has = false;
                         for (int q = 0; q < NCW; q++) {
+                            if (A_has) {
+#pragma unroll
+                                for (int k = 0; k < D * D; k++) sm.wex[b][q][k] = A.F[k];
+#pragma unroll
+                                for (int k = 0; k < D; k++) sm.wex[b][q][D * D + k] = A.c[k];
+                            }
+                            sm.wexhas[b][q] = A_has ? 1 : 0;
                             if (!sm.wthas[b][q]) continue;
                             Elem<D> e;
 #pragma unroll

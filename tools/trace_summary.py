@@ -4,11 +4,14 @@ import sys
 import numpy as np
 
 for f in sys.argv[1:]:
-    a = np.fromfile(f, dtype=np.uint64).reshape(-1, 8).astype(np.float64)
+    a = np.fromfile(f, dtype=np.uint64).reshape(-1, 16).astype(np.float64)
     a = a[a[:, 0] > 0]
     t0 = a[:, 6].min()
-    a[:, :7] -= t0
+    cols = [c for c in range(16) if c != 7]
+    a[:, cols] -= t0
     parts = (("claim->build", a[:, 0] - a[:, 6]), ("build", a[:, 1] - a[:, 0]),
+             ("  items", a[:, 8] - a[:, 0]), ("  warp scan", a[:, 9] - a[:, 8]),
+             ("  tile barrier", a[:, 10] - a[:, 9]), ("  agg publish", a[:, 1] - a[:, 10]),
              ("agg->lookback", a[:, 2] - a[:, 1]), ("lookback", a[:, 3] - a[:, 2]),
              ("pref->apply", a[:, 4] - a[:, 3]), ("apply", a[:, 5] - a[:, 4]))
     print(f, "tiles", len(a), "iteration span us", round(a[:, 5].max() / 1e3, 1))

@@ -35,7 +35,7 @@ int main(int argc, char** argv) {
     }
     void* ws; cudaMalloc(&ws, ws_bytes);
     long long ntiles = (N + 511) / 512;
-    unsigned long long* tr; cudaMalloc(&tr, ntiles * 64); cudaMemset(tr, 0, ntiles * 64);
+    unsigned long long* tr; cudaMalloc(&tr, ntiles * 128); cudaMemset(tr, 0, ntiles * 128);
     cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr));
     for (int rep = 0; rep < 2; rep++) {
         cudaMemcpy(X, h.data(), N * 16, cudaMemcpyHostToDevice);
@@ -50,8 +50,8 @@ int main(int argc, char** argv) {
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         fprintf(stderr, "rc=%d %s  ms=%.3f  ntiles=%lld\n", rc, cudaGetErrorString(cudaGetLastError()), ms, ntiles);
     }
-    std::vector<unsigned long long> ht(ntiles * 8);
-    cudaMemcpy(ht.data(), tr, ntiles * 64, cudaMemcpyDeviceToHost);
+    std::vector<unsigned long long> ht(ntiles * 16);
+    cudaMemcpy(ht.data(), tr, ntiles * 128, cudaMemcpyDeviceToHost);
     fwrite(ht.data(), 8, ht.size(), stdout);
     return 0;
 }
