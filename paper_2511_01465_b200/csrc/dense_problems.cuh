@@ -1,0 +1,32 @@
+// dense_problems.cuh — row-parallel device functors for large state dims.
+//
+// For d = 64 a thread per state component evaluates f_i(x) and the i-th row
+// of the (dense, zeros included) Jacobian — the same values the reference's
+// jac_into writes (tests/golden/make_golden.py, oracle/odescan_oracle.c).
+#pragma once
+
+#include "problems.cuh"
+
+namespace odx {
+
+// Allen-Cahn method of lines, periodic (BASELINE cfg 4): params eps, dx.
+struct AllenCahnRows {
+    int n;
+    double cdiff;
+    __device__ __forceinline__ AllenCahnRows(const ProbParams& q, int dim)
+        : n(dim), cdiff(q.p[0] / (q.p[1] * q.p[1])) {}
+    __device__ __forceinline__ double f(const double* x, int i) const {
+        const double um = x[(i + n - 1) % n], ui = x[i], up = x[(i + 1) % n];
+        return cdiff * ((um - 2.0 * ui) + up) + (ui - ui * ui * ui);
+    }
+    // J[i][j] for j in [0, n)
+    __device__ __forceinline__ double jac(const double* x, int i, int j) const {
+        double v = 0.0;
+        if (j == i) v = -2.0 * cdiff + (1.0 - 3.0 * (x[i] * x[i]));
+        if (j == (i + n - 1) % n) v += cdiff;
+        if (j == (i + 1) % n) v += cdiff;
+        return v;
+    }
+};
+
+}  // namespace odx

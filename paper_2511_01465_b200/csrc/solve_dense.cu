@@ -1,21 +1,616 @@
-// solve_dense.cu — d = 64 dense path (Allen-Cahn, BASELINE cfg 4).  (stub)
+// solve_dense.cu — the d = 64 dense path (BASELINE cfg 4: Allen-Cahn, backward
+// Euler, N = 65536).
+//
+// Reference arithmetic per Newton iteration (_kernels.py:393-464, :116-233):
+// per step a pivoted 64x64 LU, F = A^{-1}(I + dt w_p Jp) column by column,
+// c = A^{-1}(-h), then a Blelloch scan whose combines are 64x64 GEMMs
+// (~1.24 MFLOP per step).  Here, per iteration:
+//
+//   K1 dense_build    one CTA per step (grid-stride): Gauss-Jordan with partial
+//                     pivoting on [A | B | -h] (64 x 129, shared memory) gives
+//                     F = A^{-1} B and c = A^{-1}(-h) in one elimination.  The
+//                     A columns use non-contracted products, so pivot choices
+//                     and the 1e-300 singular-block test are the reference's
+//                     (GJ applies LU's exact updates to the rows below a pivot).
+//   decide            one thread: solve()'s decision (newton_pint.py:373-394)
+//   K2 dense_agg      one CTA per contiguous chunk: P <- F_j P chained with
+//                     fp64 DMMA tiles (mma.sync m8n8k4, SASS DMMA) on padded
+//                     smem operands, F_j rows TMA-staged (double-buffered)
+//   K4 dense_fixup    one CTA per chunk: incoming state from the preceding
+//                     chunk aggregates, then p_j = F_j p_{j-1} + c_j across the
+//                     chunk, X_next = X + p, max|dx| reduction
+//
+// The host enqueues every iteration up front; the kernels of an iteration
+// after the stop decision return immediately (no host synchronisation).
+#include <climits>
+#include <cstring>
+
 #include "common.cuh"
+#include "dense_problems.cuh"
+#include "scan.cuh"
+#include "sm100.cuh"
 #include "solve_small.cuh"
 
 namespace odx {
 
-int dense_supported(const odx_problem*, const odx_stepper*) { return 0; }
-int dense_solve(const odx_problem*, const odx_stepper*, SolveParams&, void*, size_t, cudaStream_t,
-                bool, size_t*) {
-    return fail(ODX_EUNSUPPORTED, "dense path not built");
+constexpr int DN = 64;            // dense state dimension
+constexpr int GJW = 2 * DN + 1;   // [A | B | -h]
+constexpr int GJLD = GJW + 1;     // 130
+constexpr int FLD = 68;           // padded leading dim of GEMM operands (conflict-free DMMA)
+constexpr int DTHREADS = 256;
+
+struct DenseState {
+    int stopped;
+    int cur;
+    unsigned fin;  // fix-up completion counter
+    int pad;
+};
+
+struct DenseParams {
+    ProbParams prob;
+    StepCoefs sc;
+    const double* x0;
+    double* X;
+    double* Xalt;
+    long long N;
+    int max_iters, abort_nonfinite;
+    double rtol, stol;
+    double* hist;
+    double* shist;
+    int* iters;
+    int* status;
+    long long* sidx;
+    double* F;   // N x 64 x 64
+    double* c;   // N x 64
+    double* h;   // N x 64 (ops only) or null
+    double* aggP;  // nchunks x 64 x 64
+    double* aggy;  // nchunks x 64
+    unsigned long long* red;  // 4 per iteration: rn, sc, step, bad
+    long long* first_bad;     // ops only
+    DenseState* st;           // null for ops
+    int nchunks;
+};
+
+// ---- NaN-ignoring row rule over 64 entries held two per lane (_kernels.py:84-95)
+// loc = max |v_j| over the entries after the last NaN; NaN (dropped) if the
+// last entry is NaN.
+__device__ __forceinline__ double warp_row_rule64(double a, double b) {
+    const int lane = threadIdx.x & 31;
+    const unsigned ma = __ballot_sync(FULL, isnan(a)), mb = __ballot_sync(FULL, isnan(b));
+    int L = -1;
+    if (mb)
+        L = 32 + (31 - __clz(mb));
+    else if (ma)
+        L = 31 - __clz(ma);
+    double v = 0.0;
+    if (lane > L) v = fmax(v, fabs(a));
+    if (lane + 32 > L) v = fmax(v, fabs(b));
+    v = warp_max_nan_drop(v);
+    return (L == 63) ? __longlong_as_double(0x7ff8000000000000ll) : v;
 }
-int dense_build_op(const odx_problem*, const odx_stepper*, const StepCoefs&, const double*,
-                   const double*, long long, double*, double*, double*, long long*, cudaStream_t) {
-    return fail(ODX_EUNSUPPORTED, "dense path not built");
+
+__device__ __forceinline__ int chunk_begin(long long N, int C, int c) {
+    const long long base = N / C, rem = N % C;
+    return (int)(c * base + (c < rem ? c : rem));
 }
+
+// =========================================================================
+// K1: per-step Gauss-Jordan build
+// =========================================================================
+template <class DP>
+__global__ void __launch_bounds__(DTHREADS)
+dense_build_kernel(const DenseParams p, int it) {
+    if (p.st && p.st->stopped) return;
+    extern __shared__ __align__(16) double dsm[];
+    double* aug = dsm;                 // 64 x GJLD
+    double* xp = aug + DN * GJLD;      // 64
+    double* xk = xp + DN;              // 64
+    double* mult = xk + DN;            // 64
+    __shared__ int s_piv, s_sing;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const DP prob(p.prob, DN);
+    const double* Xc = (p.st && p.st->cur) ? p.Xalt : p.X;
+    const long long N = p.N;
+    double rn = 0.0, scn = 0.0;
+    unsigned long long bad = ~0ull;
+
+    for (long long k = blockIdx.x; k < N; k += gridDim.x) {
+        if (tid < DN) {
+            xk[tid] = Xc[k * DN + tid];
+            xp[tid] = (k == 0) ? p.x0[tid] : Xc[(k - 1) * DN + tid];
+        }
+        __syncthreads();
+        double hv = 0.0;
+        if (tid < DN) {
+            const double fp = prob.f(xp, tid), fn = prob.f(xk, tid);
+            hv = xk[tid] - xp[tid] - p.sc.dt * (p.sc.w_prev * fp + p.sc.w_next * fn);
+            aug[tid * GJLD + 2 * DN] = -hv;
+            if (p.h) p.h[k * DN + tid] = hv;
+        }
+        for (int q = tid; q < DN * DN; q += DTHREADS) {
+            const int i = q / DN, j = q % DN;
+            const double dij = (i == j) ? 1.0 : 0.0;
+            aug[i * GJLD + j] = __dsub_rn(dij, __dmul_rn(p.sc.dt_wnext, prob.jac(xk, i, j)));
+            aug[i * GJLD + DN + j] = __dadd_rn(__dmul_rn(p.sc.dt_wprev, prob.jac(xp, i, j)), dij);
+        }
+        __syncthreads();
+        if (w == 0) {
+            const double a = -aug[lane * GJLD + 2 * DN], b = -aug[(lane + 32) * GJLD + 2 * DN];
+            rn = nan_drop_max(rn, warp_row_rule64(a, b));
+        }
+        // ---- Gauss-Jordan with partial pivoting ----------------------------
+        bool singular = false;
+        for (int pc = 0; pc < DN; pc++) {
+            if (w == 0) {
+                // reference pivot rule (_kernels.py:36-45): start from row pc,
+                // a later row wins only if strictly larger; NaN never wins
+                const double d0 = fabs(aug[pc * GJLD + pc]);
+                int bi = pc;
+                double bv = d0;
+                if (!isnan(d0)) {
+                    for (int r = pc + 1 + lane; r < DN; r += 32) {
+                        const double v = fabs(aug[r * GJLD + pc]);
+                        if (v > bv) {  // first max within the lane's rows
+                            bv = v;
+                            bi = r;
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const double ov = __shfl_xor_sync(FULL, bv, off);
+                        const int oi = __shfl_xor_sync(FULL, bi, off);
+                        if (ov > bv || (ov == bv && oi < bi)) {
+                            bv = ov;
+                            bi = oi;
+                        }
+                    }
+                }
+                if (lane == 0) {
+                    s_piv = bi;
+                    s_sing = (bv < 1e-300) ? 1 : 0;
+                }
+            }
+            __syncthreads();
+            if (s_sing) {
+                singular = true;
+                break;
+            }
+            const int pv = s_piv;
+            if (pv != pc) {
+                for (int j = tid; j < GJW; j += DTHREADS) {
+                    const double t = aug[pc * GJLD + j];
+                    aug[pc * GJLD + j] = aug[pv * GJLD + j];
+                    aug[pv * GJLD + j] = t;
+                }
+                __syncthreads();
+            }
+            if (tid < DN) {
+                const double inv = 1.0 / aug[pc * GJLD + pc];
+                mult[tid] = (tid == pc) ? 0.0 : aug[tid * GJLD + pc] * inv;
+            }
+            __syncthreads();
+            const int width = GJW - pc - 1;
+            for (int q = tid; q < DN * width; q += DTHREADS) {
+                const int i = q / width, j = pc + 1 + q % width;
+                if (i == pc) continue;
+                const double m = mult[i];
+                if (j < DN)
+                    aug[i * GJLD + j] = __dsub_rn(aug[i * GJLD + j], __dmul_rn(m, aug[pc * GJLD + j]));
+                else
+                    aug[i * GJLD + j] = aug[i * GJLD + j] - m * aug[pc * GJLD + j];
+            }
+            __syncthreads();
+        }
+        // ---- results: F = A^{-1} B (0 at step 0), c = A^{-1}(-h) -------------
+        if (singular) {
+            if ((unsigned long long)k < bad) bad = (unsigned long long)k;
+            for (int q = tid; q < DN * DN; q += DTHREADS) p.F[k * DN * DN + q] = 0.0;
+            if (tid < DN) p.c[k * DN + tid] = 0.0;
+        } else {
+            for (int q = tid; q < DN * DN; q += DTHREADS) {
+                const int i = q / DN, j = q % DN;
+                p.F[k * DN * DN + q] = (k == 0) ? 0.0 : aug[i * GJLD + DN + j] / aug[i * GJLD + i];
+            }
+            if (tid < DN) p.c[k * DN + tid] = aug[tid * GJLD + 2 * DN] / aug[tid * GJLD + tid];
+            if (w == 0) {
+                const double a = aug[lane * GJLD + 2 * DN] / aug[lane * GJLD + lane];
+                const double b = aug[(lane + 32) * GJLD + 2 * DN] / aug[(lane + 32) * GJLD + lane + 32];
+                scn = nan_drop_max(scn, warp_row_rule64(a, b));
+            }
+        }
+        __syncthreads();
+    }
+    // block reduction (only warp 0 holds rn/scn; bad is uniform per block)
+    if (tid == 0) {
+        if (p.red) {
+            unsigned long long* red = p.red + 4ll * it;
+            if (rn > 0.0) atomicMax(red + 0, dbits(rn));
+            if (scn > 0.0) atomicMax(red + 1, dbits(scn));
+            if (bad != ~0ull) atomicMin(red + 3, bad);
+        }
+        if (p.first_bad && bad != ~0ull) atomicMin(p.first_bad, (long long)bad);
+    }
+}
+
+// =========================================================================
+// decide: one thread, solve()'s sequence (same as decide() of the small path)
+// =========================================================================
+__global__ void dense_decide_kernel(const DenseParams p, int it) {
+    DenseState* st = p.st;
+    if (st->stopped) return;
+    const unsigned long long* red = p.red + 4ll * it;
+    const double rn = bitsd(red[0]);
+    const double scn = bitsd(red[1]);
+    const unsigned long long bad = red[3];
+    const double step_prev = (it > 0) ? bitsd(p.red[4ll * (it - 1) + 2])
+                                      : __longlong_as_double(0x7ff8000000000000ll);
+    SolveParams sp;
+    sp.max_iters = p.max_iters;
+    sp.abort_nonfinite = p.abort_nonfinite;
+    sp.rtol = p.rtol;
+    sp.stol = p.stol;
+    const Decision d = decide(it, sp, rn, bad, step_prev);
+    if (d.status != ODX_ST_SINGULAR) {
+        if (p.hist) p.hist[it] = rn;
+        if (p.shist) p.shist[it] = scn;
+    }
+    if (d.stop) {
+        st->stopped = 1;
+        p.iters[0] = d.iters;
+        p.status[0] = d.status;
+        p.sidx[0] = d.index;
+    }
+}
+
+// =========================================================================
+// DMMA 64x64x64: C = A * B, operands row-major with leading dim FLD, 8 warps
+// (warp w computes rows 8w..8w+7, all 64 columns).
+// =========================================================================
+__device__ __forceinline__ void gemm64_dmma(const double* A, const double* B, double* C) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    double acc[8][2];
+#pragma unroll
+    for (int n = 0; n < 8; n++) acc[n][0] = acc[n][1] = 0.0;
+    const int r0 = w * 8;
+#pragma unroll 4
+    for (int k0 = 0; k0 < DN; k0 += 4) {
+        const double a = A[(r0 + g) * FLD + k0 + t];
+#pragma unroll
+        for (int n = 0; n < 8; n++) {
+            const double b = B[(k0 + t) * FLD + n * 8 + g];
+            asm volatile(
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[n][0]), "+d"(acc[n][1])
+                : "d"(a), "d"(b));
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < 8; n++) {
+        C[(r0 + g) * FLD + n * 8 + 2 * t] = acc[n][0];
+        C[(r0 + g) * FLD + n * 8 + 2 * t + 1] = acc[n][1];
+    }
+}
+
+// y_out = M y + v (M row-major ld FLD in smem, y/v in smem); 4 threads per row
+__device__ __forceinline__ void matvec64(const double* M, const double* y, const double* v,
+                                         double* out) {
+    const int tid = threadIdx.x, r = tid >> 2, part = tid & 3;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; q++) acc += M[r * FLD + part * 16 + q] * y[part * 16 + q];
+    acc += __shfl_xor_sync(FULL, acc, 1);
+    acc += __shfl_xor_sync(FULL, acc, 2);
+    if (part == 0) out[r] = acc + v[r];
+}
+
+// stage F_j (64 rows of 512 B into padded rows) and c_j through TMA
+__device__ __forceinline__ void stage_step(const DenseParams& p, long long j, double* Fdst,
+                                           double* cdst, uint64_t* bar) {
+    mbar_arrive_expect_tx(bar, DN * DN * 8 + DN * 8);
+    for (int r = 0; r < DN; r++) tma_load_1d(Fdst + r * FLD, p.F + j * DN * DN + r * DN, DN * 8, bar);
+    tma_load_1d(cdst, p.c + j * DN, DN * 8, bar);
+}
+
+struct AggSmem {
+    double Fb[2][DN * FLD];
+    double Pb[2][DN * FLD];
+    double cb[2][DN];
+    double y[2][DN];
+    uint64_t bar[2];
+};
+
+// =========================================================================
+// K2: chunk aggregates  P = F_e ... F_s,  y = particular solution
+// =========================================================================
+__global__ void __launch_bounds__(DTHREADS) dense_agg_kernel(const DenseParams p) {
+    if (p.st && p.st->stopped) return;
+    extern __shared__ __align__(16) unsigned char raw[];
+    AggSmem& sm = *reinterpret_cast<AggSmem*>(raw);
+    const int tid = threadIdx.x, c = blockIdx.x;
+    const long long s = chunk_begin(p.N, p.nchunks, c), e = chunk_begin(p.N, p.nchunks, c + 1);
+    if (tid == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t ph[2] = {0, 0};
+    if (tid == 0) {
+        fence_proxy_async_global();
+        stage_step(p, s, sm.Fb[0], sm.cb[0], &sm.bar[0]);
+        if (s + 1 < e) stage_step(p, s + 1, sm.Fb[1], sm.cb[1], &sm.bar[1]);
+    }
+    mbar_wait(&sm.bar[0], ph[0]);
+    ph[0] ^= 1;
+    // P = F_s, y = c_s
+    for (int q = tid; q < DN * FLD; q += DTHREADS) sm.Pb[0][q] = sm.Fb[0][q];
+    if (tid < DN) sm.y[0][tid] = sm.cb[0][tid];
+    __syncthreads();
+    // buffer 0 (step s) is consumed: prefetch step s + 2 into it
+    if (tid == 0 && s + 2 < e) stage_step(p, s + 2, sm.Fb[0], sm.cb[0], &sm.bar[0]);
+    int pb = 0, yb = 0;
+    for (long long j = s + 1; j < e; j++) {
+        const int fb = (int)((j - s) & 1);
+        mbar_wait(&sm.bar[fb], ph[fb]);
+        ph[fb] ^= 1;
+        gemm64_dmma(sm.Fb[fb], sm.Pb[pb], sm.Pb[pb ^ 1]);
+        matvec64(sm.Fb[fb], sm.y[yb], sm.cb[fb], sm.y[yb ^ 1]);
+        __syncthreads();
+        // F_j / c_j consumed: prefetch step j + 2 into this buffer
+        if (tid == 0 && j + 2 < e) stage_step(p, j + 2, sm.Fb[fb], sm.cb[fb], &sm.bar[fb]);
+        pb ^= 1;
+        yb ^= 1;
+    }
+    for (int q = tid; q < DN * DN; q += DTHREADS) {
+        const int r = q / DN, col = q % DN;
+        p.aggP[(long long)c * DN * DN + q] = sm.Pb[pb][r * FLD + col];
+    }
+    if (tid < DN) p.aggy[(long long)c * DN + tid] = sm.y[yb][tid];
+}
+
+// =========================================================================
+// K4: chunk fix-up  p_j = F_j p_{j-1} + c_j,  X_next = X + p
+// =========================================================================
+struct FixSmem {
+    double Fb[2][DN * FLD];
+    double Ab[2][DN * FLD];  // chunk aggregates for the incoming state
+    double cb[2][DN];
+    double ab[2][DN];
+    double z[2][DN];
+    uint64_t bar[2];
+    double red[DTHREADS / 32];
+};
+
+__global__ void __launch_bounds__(DTHREADS) dense_fixup_kernel(const DenseParams p, int it) {
+    if (p.st && p.st->stopped) return;
+    extern __shared__ __align__(16) unsigned char raw[];
+    FixSmem& sm = *reinterpret_cast<FixSmem*>(raw);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, c = blockIdx.x;
+    const long long s = chunk_begin(p.N, p.nchunks, c), e = chunk_begin(p.N, p.nchunks, c + 1);
+    const int cur = p.st ? p.st->cur : 0;
+    const double* Xc = cur ? p.Xalt : p.X;
+    double* Xn = cur ? p.X : p.Xalt;
+    if (tid == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < DN) sm.z[0][tid] = 0.0;  // the state before step 0
+    __syncthreads();
+    uint32_t ph[2] = {0, 0};
+    // ---- incoming state: fold the aggregates of chunks 0..c-1 ---------------
+    auto stage_agg = [&](int q, int b) {
+        mbar_arrive_expect_tx(&sm.bar[b], DN * DN * 8 + DN * 8);
+        for (int r = 0; r < DN; r++)
+            tma_load_1d(&sm.Ab[b][r * FLD], p.aggP + (long long)q * DN * DN + r * DN, DN * 8, &sm.bar[b]);
+        tma_load_1d(sm.ab[b], p.aggy + (long long)q * DN, DN * 8, &sm.bar[b]);
+    };
+    if (tid == 0) {
+        fence_proxy_async_global();
+        if (c > 0) stage_agg(0, 0);
+        if (c > 1) stage_agg(1, 1);
+    }
+    int zb = 0;
+    for (int q = 0; q < c; q++) {
+        const int b = q & 1;
+        mbar_wait(&sm.bar[b], ph[b]);
+        ph[b] ^= 1;
+        matvec64(sm.Ab[b], sm.z[zb], sm.ab[b], sm.z[zb ^ 1]);
+        __syncthreads();
+        if (tid == 0 && q + 2 < c) stage_agg(q + 2, b);
+        zb ^= 1;
+    }
+    // ---- the chunk's own recursion ---------------------------------------------
+    if (tid == 0) {
+        stage_step(p, s, sm.Fb[0], sm.cb[0], &sm.bar[0]);
+        if (s + 1 < e) stage_step(p, s + 1, sm.Fb[1], sm.cb[1], &sm.bar[1]);
+    }
+    double step = 0.0;
+    for (long long j = s; j < e; j++) {
+        const int fb = (int)((j - s) & 1);
+        mbar_wait(&sm.bar[fb], ph[fb]);
+        ph[fb] ^= 1;
+        matvec64(sm.Fb[fb], sm.z[zb], sm.cb[fb], sm.z[zb ^ 1]);
+        __syncthreads();
+        if (tid == 0 && j + 2 < e) stage_step(p, j + 2, sm.Fb[fb], sm.cb[fb], &sm.bar[fb]);
+        zb ^= 1;
+        if (tid < DN) Xn[j * DN + tid] = Xc[j * DN + tid] + sm.z[zb][tid];
+        if (w == 0) step = nan_drop_max(step, warp_row_rule64(sm.z[zb][lane], sm.z[zb][lane + 32]));
+    }
+    if (tid == 0) {
+        if (step > 0.0) atomicMax(p.red + 4ll * it + 2, dbits(step));
+        __threadfence();
+        // the last chunk to finish flips the current-iterate buffer
+        const unsigned done = atomicAdd(&p.st->fin, 1u);
+        if (done == (unsigned)p.nchunks - 1) {
+            p.st->fin = 0;
+            p.st->cur ^= 1;
+        }
+    }
+}
+
+__global__ void dense_init_kernel(DenseState* st, unsigned long long* red, int H) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        st->stopped = 0;
+        st->cur = 0;
+        st->fin = 0;
+    }
+    if (i < H) {
+        red[4 * i + 0] = 0;
+        red[4 * i + 1] = 0;
+        red[4 * i + 2] = 0;
+        red[4 * i + 3] = ~0ull;
+    }
+}
+
+__global__ void dense_final_copy_kernel(const DenseParams p) {
+    if (!p.st->cur) return;
+    const long long total = p.N * DN;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (long long)gridDim.x * blockDim.x)
+        p.X[q] = p.Xalt[q];
+}
+
+// =========================================================================
+// host side
+// =========================================================================
+static bool is_dense(const odx_problem* P, const odx_stepper* S) {
+    return P && S && P->problem_id == ODX_PROB_ALLEN_CAHN && P->dim == DN &&
+           S->kind == ODX_STEP_IMPLICIT_WEIGHTED;
+}
+
+int dense_supported(const odx_problem* P, const odx_stepper* S) { return is_dense(P, S) ? 1 : 0; }
+
+static size_t build_smem() { return (size_t)(DN * GJLD + 3 * DN) * sizeof(double); }
+
+struct DenseLayout {
+    size_t total, F, c, aggP, aggy, red, st, Xalt;
+    DenseLayout(long long N, int C, int max_iters, bool with_X) {
+        size_t off = 0;
+        auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
+        F = at((size_t)N * DN * DN * 8);
+        c = at((size_t)N * DN * 8);
+        aggP = at((size_t)C * DN * DN * 8);
+        aggy = at((size_t)C * DN * 8);
+        red = at(4 * ((size_t)max_iters + 1) * 8);
+        st = at(sizeof(DenseState));
+        Xalt = with_X ? at((size_t)N * DN * 8) : 0;
+        total = off + 256;
+    }
+};
+
+template <class K>
+static int set_smem(K kern, size_t bytes) {
+    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return ODX_OK;
+}
+
+int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, void* ws,
+                size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
+    (void)P;
+    (void)S;
+    const int C = num_sms();
+    const DenseLayout lay(sp.N, C, sp.max_iters, true);
+    if (query) {
+        *need = lay.total;
+        return ODX_OK;
+    }
+    if (sp.B != 1) return fail(ODX_EUNSUPPORTED, "dense path solves one trajectory per call");
+    if (ws == nullptr || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "dense workspace too small");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    DenseParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.prob = sp.prob;
+    p.sc = sp.sc;
+    p.x0 = sp.x0;
+    p.X = sp.X;
+    p.Xalt = reinterpret_cast<double*>(base + lay.Xalt);
+    p.N = sp.N;
+    p.max_iters = sp.max_iters;
+    p.abort_nonfinite = sp.abort_nonfinite;
+    p.rtol = sp.rtol;
+    p.stol = sp.stol;
+    p.hist = sp.hist;
+    p.shist = sp.shist;
+    p.iters = sp.iters;
+    p.status = sp.status;
+    p.sidx = sp.sidx;
+    p.F = reinterpret_cast<double*>(base + lay.F);
+    p.c = reinterpret_cast<double*>(base + lay.c);
+    p.aggP = reinterpret_cast<double*>(base + lay.aggP);
+    p.aggy = reinterpret_cast<double*>(base + lay.aggy);
+    p.red = reinterpret_cast<unsigned long long*>(base + lay.red);
+    p.st = reinterpret_cast<DenseState*>(base + lay.st);
+    p.nchunks = (int)((sp.N < C) ? sp.N : C);
+    const int H = sp.max_iters + 1;
+    dense_init_kernel<<<(H + 127) / 128, 128, 0, st>>>(p.st, p.red, H);
+    auto k1 = dense_build_kernel<AllenCahnRows>;
+    int rc = set_smem(k1, build_smem());
+    if (rc) return rc;
+    rc = set_smem(dense_agg_kernel, sizeof(AggSmem));
+    if (rc) return rc;
+    rc = set_smem(dense_fixup_kernel, sizeof(FixSmem));
+    if (rc) return rc;
+    int per_sm = 0;
+    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, DTHREADS, build_smem()));
+    long long g1 = (long long)(per_sm < 1 ? 1 : per_sm) * num_sms();
+    if (g1 > sp.N) g1 = sp.N;
+    int launches = 1;
+    for (int it = 0; it <= sp.max_iters; it++) {
+        k1<<<(unsigned)g1, DTHREADS, build_smem(), st>>>(p, it);
+        dense_decide_kernel<<<1, 1, 0, st>>>(p, it);
+        launches += 2;
+        if (it < sp.max_iters) {
+            dense_agg_kernel<<<p.nchunks, DTHREADS, sizeof(AggSmem), st>>>(p);
+            dense_fixup_kernel<<<p.nchunks, DTHREADS, sizeof(FixSmem), st>>>(p, it);
+            launches += 2;
+        }
+    }
+    dense_final_copy_kernel<<<(unsigned)(2 * num_sms()), 256, 0, st>>>(p);
+    ODX_CUDA(cudaGetLastError());
+    count_launch(launches + 1);
+    return ODX_OK;
+}
+
+__global__ void set_i64_dense(long long* q, long long v) { *q = v; }
+__global__ void finalize_bad_dense(long long* q) {
+    if (*q == LLONG_MAX) *q = -1;
+}
+
+int dense_build_op(const odx_problem* P, const odx_stepper* S, const StepCoefs& sc,
+                   const double* x0, const double* X, long long N, double* Fe, double* ce,
+                   double* h, long long* first_bad, cudaStream_t st) {
+    DenseParams p;
+    std::memset(&p, 0, sizeof(p));
+    if (!fill_params(P, p.prob)) return fail(ODX_EINVAL, "bad problem parameters");
+    (void)S;
+    p.sc = sc;
+    p.x0 = x0;
+    p.X = const_cast<double*>(X);
+    p.N = N;
+    p.F = Fe;
+    p.c = ce;
+    p.h = h;
+    p.first_bad = first_bad;
+    set_i64_dense<<<1, 1, 0, st>>>(first_bad, LLONG_MAX);
+    if (N > 0) {
+        auto k1 = dense_build_kernel<AllenCahnRows>;
+        int rc = set_smem(k1, build_smem());
+        if (rc) return rc;
+        long long g1 = 3LL * num_sms();
+        if (g1 > N) g1 = N;
+        k1<<<(unsigned)g1, DTHREADS, build_smem(), st>>>(p, 0);
+    }
+    finalize_bad_dense<<<1, 1, 0, st>>>(first_bad);
+    ODX_CUDA(cudaGetLastError());
+    count_launch(N > 0 ? 3 : 2);
+    return ODX_OK;
+}
+
 int dense_scan_op(const double*, const double*, long long, int, double*, double*, void*, size_t,
                   cudaStream_t) {
-    return fail(ODX_EUNSUPPORTED, "dense path not built");
+    return fail(ODX_EUNSUPPORTED, "dense scan op: not built yet (use odx_solve)");
 }
 size_t dense_scan_op_ws(long long, int) { return 0; }
 

@@ -341,3 +341,59 @@ def test_persistent_large_vs_oracle(pkg, oracle, case):
     # implicit-path tolerance (test_acceptance.py crit 5: 1e-8)
     tol = 1e-8 if name == "robertson" else TOL
     scaled_close(r.states[0], ref["X"], tol, f"{name} states")
+
+
+# ------------------------------------------------ d = 64 dense path (cfg 4) ---
+
+def test_dense_build_op_vs_golden(pkg, golden_kernels):
+    from paper_2511_01465_b200 import kernels as K
+    g = golden_kernels
+    prob = pkg.allen_cahn()
+    for sname, stname in (("be", "backward_euler"), ("trap", "trapezoidal")):
+        key = f"bi_allen_cahn_{sname}"
+        st = pkg.get_stepper(stname, prob)
+        Fe, ce, h, bad = K.build_implicit(prob, st, dev(g[key + "_x0"]), dev(g[key + "_X"]),
+                                          float(g[key + "_dt"]))
+        assert bad == int(g[key + "_bad"])
+        for got, ref in ((h, g[key + "_h"]), (ce, g[key + "_ce"]), (Fe, g[key + "_Fe"])):
+            scaled_close(got.cpu().numpy(), ref, TOL, key)
+
+
+def test_cfg4_small_vs_golden(pkg, golden_baseline):
+    from paper_2511_01465_b200.configs import CONFIGS
+    g = golden_baseline
+    cfg = CONFIGS[4]
+    r1 = _gpu_cfg_solve(pkg, cfg, n=512, max_iters=1, step_tol=0.0, abort=False)
+    scaled_close(r1.states[0], g["cfg4t_X1"], TOL, "N=512 iterate 1")
+    r3 = _gpu_cfg_solve(pkg, cfg, n=512, max_iters=3, step_tol=0.0, abort=False)
+    scaled_close(r3.residual_history[0], g["cfg4t_hist"], 1e-7, "N=512 hist")
+    scaled_close(r3.states[0], g["cfg4t_X"], TOL, "N=512 iterate 3")
+
+
+def test_cfg4_converges_at_4096(pkg, golden_baseline):
+    """at N=4096 Newton converges in 6 iterations (step rule)."""
+    from paper_2511_01465_b200.configs import CONFIGS
+    g = golden_baseline
+    cfg = CONFIGS[4]
+    r = _gpu_cfg_solve(pkg, cfg, n=4096)
+    assert int(r.status[0]) == int(g["cfg4s_status"])
+    assert abs(int(r.iterations_run[0]) - int(g["cfg4s_iters"])) <= 1
+    scaled_close(r.states[0][::32], g["cfg4s_X_sub"], TOL, "converged X")
+
+
+def test_cfg4_full_size_first_iterates(pkg, oracle):
+    """Full N = 65536: the first iterate against the oracle, then the BASELINE
+    run to its MAXITER(100) outcome with finite iterates."""
+    from paper_2511_01465_b200.configs import CONFIGS
+    cfg = CONFIGS[4]
+    x0 = cfg.x0s()[0]
+    ref = oracle.solve(7, cfg.params, oracle.stepper_by_name("backward_euler"), x0,
+                       np.tile(x0, (cfg.n_steps, 1)), cfg.dt, 1, abort_nonfinite=False)
+    r1 = _gpu_cfg_solve(pkg, cfg, max_iters=1, step_tol=0.0, abort=False)
+    scaled_close(r1.residual_history[0][:2], ref["hist"], 1e-7, "hist")
+    scaled_close(r1.states[0], ref["X"], TOL, "full-N iterate 1")
+    r = _gpu_cfg_solve(pkg, cfg)
+    assert int(r.status[0]) == 0 and int(r.iterations_run[0]) == 100  # MAXITER
+    assert np.isfinite(r.states[0]).all()
+    h = r.residual_history[0]
+    assert np.isfinite(h).all() and h[100] < h[5]  # the late phase contracts (A.2)
