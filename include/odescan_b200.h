@@ -150,15 +150,22 @@ int odx_max_abs(const double* A, int64_t n, int32_t d, double* out, void* stream
 int odx_add_inplace(double* X, const double* U, int64_t n, int32_t d, void* stream);
 
 /* ---- time-sharded solve (one rank per GPU) ----------------------
- * Rank r owns steps [offset, offset+N_local) of one trajectory.  Per Newton
- * iteration: odx_shard_local() builds the local elements from X_local and the
- * halo state (the last state of rank r-1, or x0 on rank 0), scans them, and
- * writes a summary record of ODX_SHARD_REC(d) doubles:
- *   [F_agg (d*d) | c_agg (d) | x_last (d) | rn | sc | step_prev | bad]
- * The caller all-gathers the records (NCCL), then odx_shard_fixup() prefixes
- * the carries of ranks < r, applies the carry to the local prefixes and
- * writes X_local += dx.  Reference path: the same solve() loop
- * newton_pint.py:366-396 with the scan split across ranks.                    */
+ * Rank r owns steps [offset, offset+N_local) of one trajectory; `halo` is the
+ * state before its first step (x0 on rank 0, the last state of rank r-1
+ * otherwise).  Per Newton iteration of the reference loop
+ * (newton_pint.py:366-396):
+ *   odx_shard_local  builds the local elements (_kernels.py:299-342 /
+ *                    :393-464; F is zeroed only at the global step 0), scans
+ *                    them into the workspace and writes a record of
+ *                    ODX_SHARD_REC(d) doubles:
+ *                    [F_agg (d*d) | c_agg (d) | x_last (d) | rn | sc | step_prev | bad]
+ *                    (step_prev is NaN; the caller stores the previous step there)
+ *   (caller)         all-gathers the records (NCCL) and takes solve()'s decision
+ *   odx_shard_fixup  folds the carry of ranks < r from the gathered records,
+ *                    X_local += Fp_k z + cp_k, *step_out = max|dx| (NaN-ignoring),
+ *                    and halo += carry (rank r-1's last dx, bit-identical), so
+ *                    the halo needs no second exchange.
+ * The workspace must be the same buffer for both calls of an iteration.       */
 #define ODX_SHARD_REC(d) ((d) * (d) + 2 * (d) + 4)
 size_t odx_shard_workspace_bytes(const odx_problem* P, const odx_stepper* S,
                                  int64_t N_local);
@@ -167,7 +174,7 @@ int odx_shard_local(const odx_problem* P, const odx_stepper* S,
                     int64_t offset, double dt, double* record,
                     void* workspace, size_t workspace_bytes, void* stream);
 int odx_shard_fixup(const odx_problem* P, const double* records, int32_t rank,
-                    int32_t nranks, double* X_local, int64_t N_local,
+                    int32_t nranks, double* X_local, int64_t N_local, double* halo,
                     double* step_out, void* workspace, size_t workspace_bytes,
                     void* stream);
 

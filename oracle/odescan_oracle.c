@@ -426,9 +426,23 @@ static void rk_increment(const prob_t* P, const double* a, const double* b, int 
     }
 }
 
+/* Range variant used by the sharding tests: steps offset..offset+n-1 of a
+ * trajectory, prev of the first local step = x0 (the halo), F zeroed only at
+ * the global step 0.  offset = 0 is exactly _kernels.build_explicit. */
+void orc_build_explicit_range(int pid, int d, const double* params, const double* a,
+                              const double* b, int s, const double* x0, const double* X,
+                              int64_t n, double dt, double* Fe, double* ce, double* h,
+                              int64_t offset);
 void orc_build_explicit(int pid, int d, const double* params, const double* a, const double* b,
                         int s, const double* x0, const double* X, int64_t n, double dt,
                         double* Fe, double* ce, double* h) {
+    orc_build_explicit_range(pid, d, params, a, b, s, x0, X, n, dt, Fe, ce, h, 0);
+}
+
+void orc_build_explicit_range(int pid, int d, const double* params, const double* a,
+                              const double* b, int s, const double* x0, const double* X,
+                              int64_t n, double dt, double* Fe, double* ce, double* h,
+                              int64_t offset) {
     prob_t P = {pid, d, params};
     const int64_t dd = (int64_t)d * d;
 #pragma omp parallel for schedule(static)
@@ -445,7 +459,7 @@ void orc_build_explicit(int pid, int d, const double* params, const double* a, c
         }
         for (int r = 0; r < d; r++)
             for (int c = 0; c < d; c++)
-                Fe[k * dd + r * d + c] = (k == 0) ? 0.0 : Jg[r * d + c] + ((r == c) ? 1.0 : 0.0);
+                Fe[k * dd + r * d + c] = (offset + k == 0) ? 0.0 : Jg[r * d + c] + ((r == c) ? 1.0 : 0.0);
         free(dkap);
         free(Jg);
     }
@@ -455,9 +469,19 @@ void orc_build_explicit(int pid, int d, const double* params, const double* a, c
 /* Implicit weighted elements: _kernels.py:393-464                            */
 /* ------------------------------------------------------------------------ */
 
+int64_t orc_build_implicit_range(int pid, int d, const double* params, double w_prev,
+                                 double w_next, const double* x0, const double* X, int64_t n,
+                                 double dt, double* Fe, double* ce, double* h, int64_t offset);
 int64_t orc_build_implicit(int pid, int d, const double* params, double w_prev, double w_next,
                            const double* x0, const double* X, int64_t n, double dt,
                            double* Fe, double* ce, double* h) {
+    return orc_build_implicit_range(pid, d, params, w_prev, w_next, x0, X, n, dt, Fe, ce, h, 0);
+}
+
+/* Range variant (see orc_build_explicit_range); returned bad index is global. */
+int64_t orc_build_implicit_range(int pid, int d, const double* params, double w_prev,
+                                 double w_next, const double* x0, const double* X, int64_t n,
+                                 double dt, double* Fe, double* ce, double* h, int64_t offset) {
     prob_t P = {pid, d, params};
     const int64_t dd = (int64_t)d * d;
     int64_t worst = -1;
@@ -484,7 +508,7 @@ int64_t orc_build_implicit(int pid, int d, const double* params, double w_prev, 
                     A[r * d + c] = ((r == c) ? 1.0 : 0.0) - dt * w_next * Jn[r * d + c];
             int st = lu_factor(A, piv, d);
             if (st >= 0) {
-                if (local_bad < 0 || k < local_bad) local_bad = k;
+                if (local_bad < 0 || offset + k < local_bad) local_bad = offset + k;
                 for (int r = 0; r < d; r++) {
                     ce[k * d + r] = 0.0;
                     for (int c = 0; c < d; c++) Fe[k * dd + r * d + c] = 0.0;
@@ -494,8 +518,8 @@ int64_t orc_build_implicit(int pid, int d, const double* params, double w_prev, 
             for (int r = 0; r < d; r++) col[r] = -h[k * d + r];
             lu_solve(A, piv, col, d);
             for (int r = 0; r < d; r++) ce[k * d + r] = col[r];
-            if (k == 0) {
-                for (int64_t i = 0; i < dd; i++) Fe[i] = 0.0;
+            if (offset + k == 0) {
+                for (int64_t i = 0; i < dd; i++) Fe[k * dd + i] = 0.0;
             } else {
                 for (int c = 0; c < d; c++) {
                     for (int r = 0; r < d; r++)

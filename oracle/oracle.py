@@ -119,6 +119,11 @@ def lib():
         L.orc_build_implicit.restype = i64
         L.orc_build_implicit.argtypes = [C.c_int, C.c_int, _dp, dbl, dbl, _dp, _dp, i64, dbl,
                                          _dp, _dp, _dp]
+        L.orc_build_explicit_range.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, C.c_int, _dp,
+                                               _dp, i64, dbl, _dp, _dp, _dp, i64]
+        L.orc_build_implicit_range.restype = i64
+        L.orc_build_implicit_range.argtypes = [C.c_int, C.c_int, _dp, dbl, dbl, _dp, _dp, i64,
+                                               dbl, _dp, _dp, _dp, i64]
         L.orc_seq_explicit.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, C.c_int, _dp, dbl, i64,
                                        _dp]
         L.orc_seq_implicit.restype = i64
@@ -200,6 +205,28 @@ def build_implicit(pid, params, w_prev, w_next, x0, X, dt):
     h = np.empty((n, d))
     bad = lib().orc_build_implicit(pid, d, _params(params), float(w_prev), float(w_next),
                                    _f64(x0), X, n, float(dt), Fe, ce, h)
+    return Fe, ce, h, int(bad)
+
+
+def build_range(pid, params, stepper: Stepper, halo, X, dt, offset):
+    """Elements of steps offset.. of a trajectory (sharding tests): prev of the
+    first local step is `halo`; F is zeroed only at the global step 0."""
+    X = _f64(X)
+    n, d = X.shape
+    Fe = np.empty((n, d, d))
+    ce = np.empty((n, d))
+    h = np.empty((n, d))
+    if stepper.kind == EXPLICIT:
+        s = stepper.stages
+        a = np.array([stepper.a[i] for i in range(s * s)]).reshape(s, s)
+        b = np.array([stepper.b[i] for i in range(s)])
+        lib().orc_build_explicit_range(pid, d, _params(params), a, b, s, _f64(halo), X, n,
+                                       float(dt), Fe, ce, h, int(offset))
+        bad = -1
+    else:
+        bad = lib().orc_build_implicit_range(pid, d, _params(params), stepper.w_prev,
+                                             stepper.w_next, _f64(halo), X, n, float(dt), Fe, ce,
+                                             h, int(offset))
     return Fe, ce, h, int(bad)
 
 

@@ -97,7 +97,7 @@ def lib():
     L.odx_shard_local.restype = C.c_int
     L.odx_shard_local.argtypes = [P_, S_, vp, vp, i64, i64, dbl, vp, vp, sz, vp]
     L.odx_shard_fixup.restype = C.c_int
-    L.odx_shard_fixup.argtypes = [P_, vp, i32, i32, vp, i64, vp, vp, sz, vp]
+    L.odx_shard_fixup.argtypes = [P_, vp, i32, i32, vp, i64, vp, vp, vp, sz, vp]
     if L.odx_abi_version() != 1:
         raise RuntimeError("libodescan_b200 ABI version mismatch")
     _lib = L

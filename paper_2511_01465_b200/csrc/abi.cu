@@ -23,7 +23,7 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
 template <class P, int KIND, int S>
 int build_op(const ProbParams& pp, const StepCoefs& sc, const double* x0, const double* X,
              long long N, double* Fe, double* ce, double* h, long long* first_bad,
-             cudaStream_t st);
+             cudaStream_t st, long long offset);
 int scan_op(const double* F, const double* c, long long N, int d, double* Fp, double* cp,
             void* ws, size_t ws_bytes, cudaStream_t st);
 size_t scan_op_ws(long long N, int d);
@@ -87,10 +87,11 @@ struct BuildFn {
     double *Fe, *ce, *h;
     long long* fb;
     cudaStream_t st;
+    long long offset = 0;
     template <class PP>
     int operator()() {
         return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
-            return build_op<Q, K, SS>(*pp, *sc, x0, X, N, Fe, ce, h, fb, st);
+            return build_op<Q, K, SS>(*pp, *sc, x0, X, N, Fe, ce, h, fb, st, offset);
         });
     }
 };
@@ -188,9 +189,28 @@ int odx_solve(const odx_problem* P, const odx_stepper* S, const double* x0, doub
     return solve_impl(P, S, p, workspace, workspace_bytes, (cudaStream_t)stream, false, nullptr);
 }
 
+}  // extern "C"
+
+namespace odx {
+int build_common_offset(const odx_problem* P, const odx_stepper* S, int kind, const double* x0,
+                        const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,
+                        int64_t* first_bad, void* stream, long long offset);
+}
+
+extern "C" {
+
 static int build_common(const odx_problem* P, const odx_stepper* S, int kind, const double* x0,
                         const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,
                         int64_t* first_bad, void* stream) {
+    return odx::build_common_offset(P, S, kind, x0, X, N, dt, Fe, ce, h, first_bad, stream, 0);
+}
+
+}  // extern "C"
+
+namespace odx {
+int build_common_offset(const odx_problem* P, const odx_stepper* S, int kind, const double* x0,
+                        const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,
+                        int64_t* first_bad, void* stream, long long offset) {
     g_err.clear();
     int rc = check_problem(P, S);
     if (rc) return rc;
@@ -206,10 +226,13 @@ static int build_common(const odx_problem* P, const odx_stepper* S, int kind, co
     if (dense_supported(P, S))
         return dense_build_op(P, S, sc, x0, X, N, Fe, ce, h,
                               reinterpret_cast<long long*>(first_bad), st);
-    return with_small_problem(P->problem_id, P->dim,
-                              BuildFn{S, &pp, &sc, x0, X, N, Fe, ce, h,
-                                  reinterpret_cast<long long*>(first_bad), st});
+    BuildFn fn{S, &pp, &sc, x0, X, N, Fe, ce, h, reinterpret_cast<long long*>(first_bad), st};
+    fn.offset = offset;
+    return with_small_problem(P->problem_id, P->dim, fn);
 }
+}  // namespace odx
+
+extern "C" {
 
 int odx_build_explicit(const odx_problem* P, const odx_stepper* S, const double* x0,
                        const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,

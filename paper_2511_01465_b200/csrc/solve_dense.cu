@@ -616,14 +616,3 @@ size_t dense_scan_op_ws(long long, int) { return 0; }
 
 }  // namespace odx
 
-extern "C" {
-size_t odx_shard_workspace_bytes(const odx_problem*, const odx_stepper*, int64_t) { return 0; }
-int odx_shard_local(const odx_problem*, const odx_stepper*, const double*, const double*, int64_t,
-                    int64_t, double, double*, void*, size_t, void*) {
-    return ODX_EUNSUPPORTED;
-}
-int odx_shard_fixup(const odx_problem*, const double*, int32_t, int32_t, double*, int64_t, double*,
-                    void*, size_t, void*) {
-    return ODX_EUNSUPPORTED;
-}
-}

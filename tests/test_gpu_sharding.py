@@ -1,0 +1,115 @@
+"""GPU checks of the multi-GPU paths on ONE device.
+
+* emulated ranks: R DeviceShard objects (odx_shard_local / odx_shard_fixup)
+  on one GPU, records concatenated in place of the all-gather; the protocol is
+  bulk-synchronous, so no kernel waits on another rank's kernel
+* the real torch.distributed/NCCL drivers at world size 1
+Both must reproduce the single-GPU solve and the oracle.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False):
+    from paper_2511_01465_b200.sharded import DeviceShard, ShardedNewton, chunk_bounds
+    n, d = guess.shape
+    shards = []
+    for r in range(R):
+        off, nl = chunk_bounds(n, R, r)
+        X = torch.from_numpy(np.ascontiguousarray(guess[off:off + nl])).cuda()
+        halo = torch.from_numpy(prob.x0 if r == 0 else guess[off - 1]).cuda()
+        shards.append(DeviceShard(prob, st, dt, X, halo, off, r, R))
+
+    class Lockstep:
+        """All R ranks behind one backend: local() of every rank, then fixups."""
+        def __init__(self):
+            self.steps = [float("nan")] * R
+
+        def local(self, it):
+            return [s.local(it).clone() for s in shards]
+
+        def fixup(self, recs):
+            for s in shards:
+                s.fixup(recs)
+            self.steps = [s.step() for s in shards]
+
+        def step(self):
+            return self.steps
+
+    be = Lockstep()
+
+    def gather(recs, step_locals):
+        out = torch.stack(recs).cpu().numpy()
+        if isinstance(step_locals, list):
+            out[:, d * d + 2 * d + 2] = step_locals
+        return out
+
+    res = ShardedNewton(be, gather, d, max_iters, 0.0, step_tol, abort).run()
+    X = np.concatenate([s.X.cpu().numpy() for s in shards])
+    return X, res
+
+
+@pytest.mark.parametrize("case", [
+    ("vdp1_rk4", 1.0, "rk4", 1e-3, 20000, 10, 0.0, False),
+    ("vdp10_be", 10.0, "backward_euler", 1e-3, 65536, 100, 1e-10, True),
+])
+@pytest.mark.parametrize("R", [2, 3, 8])
+def test_emulated_time_sharding(oracle, case, R):
+    import paper_2511_01465_b200 as pkg
+    name, mu, sname, dt, n, iters, stol, abort = case
+    prob = pkg.van_der_pol(mu=mu, x0=(2.0, 0.0), tf=n * dt)
+    st = pkg.get_stepper(sname, prob)
+    guess = np.tile(prob.x0, (n, 1))
+    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, stol, abort)
+    ref = oracle.solve(1, (mu,), oracle.stepper_by_name(sname), prob.x0, guess, dt, iters,
+                       step_tol=stol, abort_nonfinite=abort)
+    assert res["status"] == ref["status"]
+    assert abs(res["iters"] - ref["iters"]) <= 1
+    h = np.array(res["hist"])
+    np.testing.assert_allclose(h[:2], ref["hist"][:2], rtol=1e-7)
+    if ref["status"] != oracle.ST_NONFINITE:
+        fin = np.isfinite(ref["X"]).all(axis=1)
+        assert np.array_equal(fin, np.isfinite(X).all(axis=1))
+        scale = max(1.0, float(np.abs(ref["X"][fin]).max()))
+        assert np.abs(X[fin] - ref["X"][fin]).max() <= 1e-9 * scale
+
+
+def test_nccl_drivers_world_size_one(oracle):
+    import torch.distributed as dist
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200.configs import CONFIGS
+    from paper_2511_01465_b200.sharded import solve_batch_sharded, solve_time_sharded
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n, dt = 8192, 1e-3
+        prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
+        st = pkg.get_stepper("rk4", prob)
+        X = torch.from_numpy(np.tile(prob.x0, (n, 1))).cuda()
+        conf = pkg.NewtonConfig(max_iters=4, abort_on_nonfinite=False)
+        rep = solve_time_sharded(prob, st, dt, X, 0, conf)
+        ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), prob.x0,
+                           np.tile(prob.x0, (n, 1)), dt, 4, abort_nonfinite=False)
+        assert rep.iterations_run == 4
+        scale = max(1.0, float(np.abs(ref["X"]).max()))
+        assert np.abs(X.cpu().numpy() - ref["X"]).max() <= 1e-9 * scale
+        cfg = CONFIGS[3]
+        lor = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=cfg.n_steps * cfg.dt)
+        local, off, gathered = solve_batch_sharded(lor, pkg.get_stepper("rk4", lor), cfg.dt,
+                                                   cfg.x0s()[:64],
+                                                   pkg.NewtonConfig(max_iters=100,
+                                                                    step_tol=1e-10))
+        assert off == 0 and gathered["status"].shape == (64,)
+        assert (gathered["status"] == 2).all()  # NONFINITE(1), SURVEY A.1
+    finally:
+        dist.destroy_process_group()

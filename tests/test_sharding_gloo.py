@@ -1,0 +1,125 @@
+"""Multi-rank paths on the CPU: world_size-2 gloo runs of the sharding protocol.
+
+The time-sharded protocol (paper_2511_01465_b200/sharded.py: local build+scan,
+one all-gather of records per Newton iteration, identical decisions, carry
+fix-up, halo += carry) runs with the oracle backend on two gloo ranks and must
+reproduce the unsharded oracle solve (newton_pint.py:366-396 semantics):
+statuses and iteration counts exactly, iterates to 1e-9 scaled.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASES = {
+    # name: (pid, params, stepper, x0, N, dt, max_iters, step_tol, abort)
+    "vdp1_rk4_fixed": (1, (1.0,), "rk4", [2.0, 0.0], 1001, 1e-3, 5, 0.0, False),
+    "vdp10_be_stop": (1, (10.0,), "backward_euler", [2.0, 0.0], 4096, 1e-3, 100, 1e-10, True),
+    "lorenz_cfg1": (6, (10.0, 28.0, 8.0 / 3.0), "rk4", [1.0, 1.0, 1.0], 1024, 0.01, 100, 1e-10,
+                    True),
+    "logistic_converge": (0, (1.0, 1.0), "rk4", [0.1], 1000, 1e-2, 11, 1e-10, True),
+}
+# initial guess per case (default: replicate x0); the logistic case uses the
+# reference's own convergent "ones" guess (tests/test_acceptance.py crit 3)
+GUESS_ONES = {"logistic_converge"}
+
+
+def _worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from _oracle_shard import OracleShard
+        from oracle import oracle as O
+        from paper_2511_01465_b200.sharded import ShardedNewton, chunk_bounds
+        pid, params, sname, x0, n, dt, max_iters, step_tol, abort = CASES[case]
+        x0 = np.asarray(x0, np.float64)
+        off, nl = chunk_bounds(n, world, rank)
+        guess = np.ones((n, x0.shape[0])) if case in GUESS_ONES else np.tile(x0, (n, 1))
+        halo = x0 if rank == 0 else guess[off - 1]
+        be = OracleShard(pid, params, O.stepper_by_name(sname), dt, guess[off:off + nl], halo,
+                         off, rank, world)
+        d = x0.shape[0]
+
+        def gather(rec, step_local):
+            r = torch.as_tensor(np.asarray(rec, np.float64).copy())
+            r[d * d + 2 * d + 2] = step_local
+            out = [torch.empty_like(r) for _ in range(world)]
+            dist.all_gather(out, r)
+            return torch.stack(out).numpy()
+
+        out = ShardedNewton(be, gather, d, max_iters, 0.0, step_tol, abort).run()
+        q.put((rank, off, be.X, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_time_sharded_protocol_gloo(oracle, case):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda t: t[0])
+    X = np.concatenate([r[2] for r in res])
+    outs = [r[3] for r in res]
+    assert outs[0]["status"] == outs[1]["status"] and outs[0]["iters"] == outs[1]["iters"]
+    pid, params, sname, x0, n, dt, max_iters, step_tol, abort = CASES[case]
+    x0 = np.asarray(x0, np.float64)
+    guess = np.ones((n, x0.shape[0])) if case in GUESS_ONES else np.tile(x0, (n, 1))
+    ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), x0, guess, dt,
+                       max_iters, step_tol=step_tol, abort_nonfinite=abort)
+    assert outs[0]["status"] == ref["status"]
+    assert outs[0]["iters"] == ref["iters"]
+    hist = np.array(outs[0]["hist"])
+    np.testing.assert_allclose(hist, ref["hist"][: len(hist)], rtol=1e-7, atol=0)
+    if ref["status"] != oracle.ST_NONFINITE:
+        fin = np.isfinite(ref["X"])
+        scale = max(1.0, float(np.abs(ref["X"][fin]).max()))
+        assert np.abs(X[fin] - ref["X"][fin]).max() <= 1e-9 * scale
+
+
+def test_chunk_bounds_partition():
+    from paper_2511_01465_b200.sharded import chunk_bounds
+    for n in (1, 7, 64, 1001):
+        for R in (1, 2, 3, 8):
+            if R > n:
+                continue
+            spans = [chunk_bounds(n, R, r) for r in range(R)]
+            assert spans[0][0] == 0
+            for (o1, n1), (o2, _) in zip(spans, spans[1:]):
+                assert o1 + n1 == o2
+            assert sum(s[1] for s in spans) == n
+            assert max(s[1] for s in spans) - min(s[1] for s in spans) <= 1
+
+
+def test_decide_matches_oracle_semantics():
+    from paper_2511_01465_b200 import _native as N
+    from paper_2511_01465_b200.sharded import decide
+    nan = float("nan")
+    assert decide(0, 5, 0.0, 0.0, True, 1.0, 3, nan) == (True, N.ST_SINGULAR, 3, 0)
+    assert decide(2, 5, 0.0, 0.0, True, float("inf"), -1, 1.0) == (True, N.ST_NONFINITE, 2, 2)
+    assert decide(2, 5, 0.0, 0.0, False, float("inf"), -1, 1.0)[0] is False
+    assert decide(5, 5, 0.0, 0.0, True, 1.0, -1, 1.0) == (True, N.ST_MAXITER, -1, 5)
+    assert decide(3, 5, 1e-6, 0.0, True, 1e-7, -1, 1.0) == (True, N.ST_CONVERGED, -1, 3)
+    assert decide(3, 5, 0.0, 1e-10, True, 1.0, -1, 1e-11) == (True, N.ST_CONVERGED, -1, 3)
+    assert decide(0, 5, 0.0, 1e-10, True, 1.0, -1, nan)[0] is False
