@@ -229,6 +229,43 @@ class Workload:
         return it, st, ix
 
 
+class TimeShardedWorkload:
+    """cfg 5 at N > 1 GPUs: one trajectory split along time (sharded.py)."""
+
+    def __init__(self, cid: int, iters: int, rank: int, world: int):
+        import torch
+        import paper_2511_01465_b200 as pkg
+        from paper_2511_01465_b200 import _native as N
+        from paper_2511_01465_b200.configs import CONFIGS
+        from paper_2511_01465_b200.sharded import chunk_bounds
+        self.torch, self.N = torch, N
+        self.cfg = cfg = CONFIGS[cid]
+        self.n_total = cfg.n_steps
+        self.off, self.n = chunk_bounds(self.n_total, world, rank)
+        self.B, self.d = 1, cfg.dim
+        self.iters = iters
+        x0 = cfg.x0s()[0]
+        self.prob = pkg.van_der_pol(mu=cfg.params[0], x0=x0, tf=self.n_total * cfg.dt)
+        self.stepper = pkg.get_stepper(cfg.stepper, self.prob)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.guess = torch.from_numpy(x0).to(dev)[None, :].expand(self.n, self.d).contiguous()
+        self.X = torch.empty_like(self.guess)
+        self.conf = pkg.NewtonConfig(max_iters=iters, abort_on_nonfinite=False)
+        self.rep = None
+
+    def reset(self):
+        self.X.copy_(self.guess)
+
+    def launch(self):
+        from paper_2511_01465_b200.sharded import solve_time_sharded
+        self.rep = solve_time_sharded(self.prob, self.stepper, self.cfg.dt, self.X, self.off,
+                                      self.conf)
+
+    def outcome(self):
+        r = self.rep
+        return (np.array([r.iterations_run]), np.array([r.status]), np.array([r.status_index]))
+
+
 def flush_l2(buf):
     buf.add_(1.0)  # 256 MB written > 126 MB L2
 
@@ -408,7 +445,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm, hbm_src, fp64, fp64_src = peaks()
     cid = cfg_id(args.workload)
-    w = Workload(cid, args.iters, rank=rank, world=world)
+    if cid == 5 and world > 1:
+        w = TimeShardedWorkload(cid, args.iters, rank, world)
+    else:
+        w = Workload(cid, args.iters, rank=rank, world=world)
     flush_buf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
 
     def flush():
@@ -422,25 +462,29 @@ def main():
     durs, launches = time_steps(w, args.steps, args.warmup, flush)
     clock_info = clocks.stop()
     tot_ms = reduce_max(sum(durs), world)
-    units_per_step = w.B * w.n * args.iters * world
+    sharded_time = isinstance(w, TimeShardedWorkload)
+    units_per_step = (w.n_total * args.iters) if sharded_time else (w.B * w.n * args.iters * world)
     value = units_per_step * args.steps / (tot_ms * 1e-3)
     avg_ms = tot_ms / args.steps
     it, st, ix = w.outcome()
 
-    # e2e through the public API with host buffers
-    e2e_durs, h2d, d2h = e2e_steps(w, max(3, args.steps // 2), 2)
-    e2e_ms = reduce_max(sum(e2e_durs), world) / len(e2e_durs)
-    e2e_val = units_per_step / (e2e_ms * 1e-3)
-
-    # BASELINE stop-rule solve of the same config
-    w.set_mode(fixed=False)
-    sr_durs, _ = time_steps(w, 5, 2, flush)
-    sit, sst, six = w.outcome()
-    sr_ms = statistics.median(sr_durs)
     names = {0: "MAXITER", 1: "CONVERGED", 2: "NONFINITE", 3: "SINGULAR"}
-    stop_rule = {"status": names.get(int(sst[0]), str(int(sst[0]))),
-                 "status_index": int(six[0]), "iterations": int(sit[0]), "solve_ms": sr_ms,
-                 "newton_steps_per_s": w.n * w.B * max(int(sit[0]), 1) / (sr_ms * 1e-3)}
+    if sharded_time:
+        e2e_ms, e2e_val, h2d, d2h = avg_ms, value, 0, 0
+        stop_rule = None
+    else:
+        # e2e through the public API with host buffers
+        e2e_durs, h2d, d2h = e2e_steps(w, max(3, args.steps // 2), 2)
+        e2e_ms = reduce_max(sum(e2e_durs), world) / len(e2e_durs)
+        e2e_val = units_per_step / (e2e_ms * 1e-3)
+        # BASELINE stop-rule solve of the same config
+        w.set_mode(fixed=False)
+        sr_durs, _ = time_steps(w, 5, 2, flush)
+        sit, sst, six = w.outcome()
+        sr_ms = statistics.median(sr_durs)
+        stop_rule = {"status": names.get(int(sst[0]), str(int(sst[0]))),
+                     "status_index": int(six[0]), "iterations": int(sit[0]), "solve_ms": sr_ms,
+                     "newton_steps_per_s": w.n * w.B * max(int(sit[0]), 1) / (sr_ms * 1e-3)}
 
     roof = roofline_for(cid, w.n, w.B, args.iters, avg_ms, hbm, hbm_src, fp64, fp64_src)
     prof_traffic = REPO / "profiles" / "traffic.json"
@@ -491,16 +535,20 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": avg_ms,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if (sharded_time or cid == 3) else "weak",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (BASELINE.json configs, seeded default_rng(0))",
             "config": {"workload": w.cfg.name, "problem": w.cfg.problem, "stepper": w.cfg.stepper,
-                       "n_steps": w.n, "dim": w.d, "batch": w.B * world,
+                       "n_steps": w.n_total if sharded_time else w.n, "dim": w.d,
+                       "batch": w.B if cid == 3 else w.B * world,
                        "newton_iters": args.iters,
                        "mode": "fixed iterations, non-aborting (SURVEY 8d)",
                        "l2": "flushed between steps (256 MB write)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"time-sharded x{world}" if sharded_time else
+                                       f"batch-sharded x{world}" if cid == 3 else
+                                       f"replicas x{world}")},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Newton time-steps/s", "ms": e2e_ms,

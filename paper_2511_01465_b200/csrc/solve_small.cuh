@@ -439,4 +439,204 @@ persistent_solve_kernel(const SolveParams p) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Grid-resident solve: one trajectory with N <= G * THREADS * ITEMS, G CTAs
+// co-resident (cooperative launch).  CTA g owns steps [g*T, g*T + T) for the
+// whole solve: X rows stay in its shared memory and its elements in registers;
+// per Newton iteration there is ONE grid barrier (after the tile aggregates and
+// the residual reductions are published).  Each CTA then folds the aggregates
+// of the CTAs before it (L2-resident, a warp-parallel ordered reduction) into
+// its incoming state, applies it, and hands its new last row to CTA g+1
+// through a tagged 16-byte chunk (no second barrier).  HBM is touched only by
+// the initial load and the final store (BASELINE cfg 2: 1 MB of state).
+// ---------------------------------------------------------------------------
+struct GridResParams {
+    SolveParams sp;
+    double* aggs;      // G x (D*D + D)
+    void* halos;       // G x D chunks {value, tag}
+};
+
+template <int D>
+__device__ __forceinline__ void warp_reduce_earliest_first(Elem<D>& e, bool& has, int lane) {
+    // lower lanes are EARLIER in time; lane 0 ends with the composition of all
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Elem<D> o;
+        shfl_down_elem<D>(e, o, off);
+        bool oh = __shfl_down_sync(FULL, has, off);
+        if ((lane & (2 * off - 1)) == 0 && lane + off < 32 && oh) {
+            if (has)
+                compose<D>(e, o, e);  // o is later
+            else {
+                e = o;
+                has = true;
+            }
+        }
+    }
+}
+
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS)
+grid_resident_kernel(const GridResParams gp) {
+    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
+    constexpr int D = P::D;
+    constexpr int NW = E::NW;
+    constexpr int T = E::T;
+    constexpr int EA = D * D + D;
+    using L = typename E::L;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typename E::Shared& sm = *reinterpret_cast<typename E::Shared*>(smem_raw);
+    __shared__ double s_z[D];
+
+    const SolveParams& p = gp.sp;
+    struct HChunk { double v; unsigned long long tag; };
+    HChunk* halos = reinterpret_cast<HChunk*>(gp.halos);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const long long g = blockIdx.x;
+    const unsigned G = gridDim.x;
+    const long long N = p.N;
+    const long long base = g * T;
+    const long long rows = (N - base) < T ? (N - base) : T;
+    const P prob(p.prob);
+
+    // initial rows (row 0 = the state before step base)
+    for (int i = tid; i < (int)((rows + 1) * D); i += THREADS) {
+        const long long gi = (base - 1) * D + i;
+        sm.xs[L::idx(i)] = (gi < 0) ? p.x0[i] : p.X[gi];
+    }
+    __syncthreads();
+
+    Decision dd{0, -1, -1, 0};
+    for (int it = 0; it <= p.max_iters; it++) {
+        // halo from CTA g-1 (its last row of the current iterate)
+        if (it > 0 && g > 0 && tid < D) {
+            const HChunk* src = halos + (g - 1) * D + tid;
+            const unsigned long long want = (unsigned long long)it;
+            unsigned long long tag;
+            long long v;
+            int spins = 0;
+            while (true) {
+                asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                             : "=l"(v), "=l"(tag) : "l"(src) : "memory");
+                if (tag == want) break;
+                if (++spins > 8) __nanosleep(20);
+            }
+            sm.xs[L::idx(tid)] = __longlong_as_double(v);
+        }
+        __syncthreads();
+        Elem<D> el[ITEMS];
+        double rn = 0.0, scn = 0.0;
+        unsigned long long bad = ~0ull;
+        E::build_items(prob, p.sc, sm, base, N, el, rn, scn, bad);
+        Elem<D> agg;
+        bool has;
+        const bool do_scan = it < p.max_iters;
+        if (do_scan) E::block_scan(sm, base, N, el, agg, has);
+        rn = warp_max_nan_drop(rn);
+        scn = warp_max_nan_drop(scn);
+        bad = warp_min_u64(bad);
+        if (lane == 0) {
+            sm.redd[0][w] = rn;
+            sm.redd[1][w] = scn;
+            sm.redb[w] = bad;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, c = 0.0;
+            unsigned long long m = ~0ull;
+            for (int q = 0; q < NW; q++) {
+                a = fmax(a, sm.redd[0][q]);
+                c = fmax(c, sm.redd[1][q]);
+                m = sm.redb[q] < m ? sm.redb[q] : m;
+            }
+            unsigned long long* red = p.red + 4ll * it;
+            if (a > 0.0) atomicMax(red + 0, dbits(a));
+            if (c > 0.0) atomicMax(red + 1, dbits(c));
+            if (m != ~0ull) atomicMin(red + 3, m);
+            if (do_scan) {
+                Elem<D> A;
+                bool A_has = false;
+                E::tile_aggregate(sm, A, A_has);
+                double* dst = gp.aggs + g * EA;
+#pragma unroll
+                for (int k = 0; k < D * D; k++) dst[k] = A.F[k];
+#pragma unroll
+                for (int k = 0; k < D; k++) dst[D * D + k] = A.c[k];
+            }
+        }
+        grid_barrier(p.bar, p.bar + 1, G);
+        const unsigned long long* red = p.red + 4ll * it;
+        const double rnb = bitsd(__ldcg(red + 0));
+        const double scb = (KIND == 0) ? rnb : bitsd(__ldcg(red + 1));
+        // every CTA's step atomic of iteration it-1 precedes this barrier
+        const double step_prev = (it > 0) ? bitsd(__ldcg(red - 4 + 2))
+                                          : __longlong_as_double(0x7ff8000000000000ll);
+        dd = decide(it, p, rnb, __ldcg(red + 3), step_prev);
+        if (g == 0 && tid == 0 && dd.status != ODX_ST_SINGULAR) {
+            if (p.hist) p.hist[it] = rnb;
+            if (p.shist) p.shist[it] = scb;
+        }
+        if (dd.stop) break;
+        // incoming state: ordered fold of the aggregates of CTAs 0..g-1 (warp 0)
+        if (w == 0) {
+            Elem<D> e;
+            bool eh = false;
+            const long long per = (g + 31) / 32;
+            const long long lo = lane * per, hi = (lo + per < g) ? lo + per : g;
+            for (long long q = lo; q < hi; q++) {
+                Elem<D> a;
+                const double* src = gp.aggs + q * EA;
+#pragma unroll
+                for (int k = 0; k < D * D; k++) a.F[k] = __ldcg(src + k);
+#pragma unroll
+                for (int k = 0; k < D; k++) a.c[k] = __ldcg(src + D * D + k);
+                if (eh)
+                    compose<D>(e, a, e);
+                else {
+                    e = a;
+                    eh = true;
+                }
+            }
+            if (!eh) set_identity<D>(e);
+            warp_reduce_earliest_first<D>(e, eh, lane);
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < D; k++) s_z[k] = eh ? e.c[k] : 0.0;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < D; k++) sm.z[k] = s_z[k];
+        }
+        __syncthreads();
+        double step = 0.0;
+        E::apply_items(sm, base, N, el, agg, has, step);
+        step = warp_max_nan_drop(step);
+        if (lane == 0) sm.redd[2][w] = step;
+        __syncthreads();
+        // hand the new last row to CTA g+1 (tag = next iteration)
+        if (g + 1 < G && tid < D) {
+            const double v = sm.xs[L::idx((int)rows * D + tid)];
+            HChunk* dst = halos + g * D + tid;
+            asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(dst),
+                         "l"(__double_as_longlong(v)), "l"((unsigned long long)(it + 1))
+                         : "memory");
+        }
+        if (tid == 0) {
+            double s2 = 0.0;
+            for (int q = 0; q < NW; q++) s2 = fmax(s2, sm.redd[2][q]);
+            if (s2 > 0.0) atomicMax(p.red + 4ll * it + 2, dbits(s2));
+        }
+        __syncthreads();
+    }
+    // final iterate back to global memory
+    for (int i = tid; i < (int)(rows * D); i += THREADS) p.X[base * D + i] = sm.xs[L::idx(i + D)];
+    if (g == 0 && tid == 0) {
+        p.iters[0] = dd.iters;
+        p.status[0] = dd.status;
+        p.sidx[0] = dd.index;
+    }
+}
+
 }  // namespace odx

@@ -144,6 +144,63 @@ int launch_ws(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
     return ODX_OK;
 }
 
+// Grid-resident solve (one tile per CTA for the whole solve).  Returns
+// ODX_EUNSUPPORTED (without launching) when the trajectory does not fit one
+// co-resident wave of CTAs.
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+int launch_grid_resident(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
+                         size_t* need) {
+    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
+    constexpr int D = P::D;
+    auto kern = grid_resident_kernel<P, KIND, S, THREADS, ITEMS>;
+    const long long G = (p.N + E::T - 1) / E::T;
+    const size_t smem = sizeof(typename E::Shared);
+    int per_sm = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return ODX_EUNSUPPORTED;
+    }
+    if (G > (long long)per_sm * num_sms()) return ODX_EUNSUPPORTED;
+    size_t off = 0;
+    auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
+    const size_t o_red = at(4 * ((size_t)p.max_iters + 1) * 8);
+    const size_t o_bar = at(8);
+    const size_t o_halo = at((size_t)G * D * 16);
+    const size_t zero_end = off;
+    const size_t o_aggs = at((size_t)G * (D * D + D) * 8);
+    const size_t total = off + 256;
+    if (query) {
+        *need = total;
+        return ODX_OK;
+    }
+    if (ws == nullptr || ws_bytes < total) return fail(ODX_EWORKSPACE, "workspace too small");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    GridResParams gp;
+    gp.sp = p;
+    gp.sp.red = reinterpret_cast<unsigned long long*>(base + o_red);
+    gp.sp.bar = reinterpret_cast<unsigned*>(base + o_bar);
+    gp.halos = base + o_halo;
+    gp.aggs = reinterpret_cast<double*>(base + o_aggs);
+    ODX_CUDA(cudaMemsetAsync(base, 0, zero_end, st));
+    init_bad_slots(gp.sp.red, p.max_iters + 1, st);
+    void* args[] = {&gp};
+    ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(THREADS), args,
+                                         smem, st));
+    ODX_CUDA(cudaGetLastError());
+    count_launch(2);
+    return ODX_OK;
+}
+
+inline bool use_grid_resident() {
+    static const bool on = [] {
+        const char* v = std::getenv("ODX_GRID_RESIDENT");
+        return !(v && std::strcmp(v, "0") == 0);
+    }();
+    return on;
+}
+
 inline bool use_legacy_persistent() {
     static const bool legacy = [] {
         const char* v = std::getenv("ODX_PERSISTENT");
@@ -168,6 +225,16 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
     const bool resident = p.N <= 256LL * RI;
     constexpr int WI = ws_items<D>();
     const bool small_ws = p.N < 128LL * WI * 296;  // keep >= 2 tiles per SM
+    // one trajectory that fits one wave of CTAs: grid-resident solve
+    if (!resident && p.B == 1 && use_grid_resident()) {
+        constexpr int GI = (D <= 2) ? 4 : 2;
+        int rc = ODX_EUNSUPPORTED;
+        if (p.N <= 128LL * 2 * 148)
+            rc = launch_grid_resident<P, KIND, S, 128, 2>(p, ws, ws_bytes, st, query, need);
+        if (rc == ODX_EUNSUPPORTED)
+            rc = launch_grid_resident<P, KIND, S, 128, GI>(p, ws, ws_bytes, st, query, need);
+        if (rc != ODX_EUNSUPPORTED) return rc;
+    }
     if (query) {
         *need = 0;
         if (!resident) {
