@@ -213,32 +213,106 @@ def _device(device):
     return device
 
 
+class _Buffers:
+    """Per-device grow-only caches: solver workspace, packed outcome buffer and
+    pinned host staging (avoids per-call allocation, fill kernels and pageable
+    copies on the end-to-end path)."""
+
+    def __init__(self):
+        self.ws = {}
+        self.pinned = {}
+
+    def workspace(self, dev, nbytes):
+        import torch
+        buf = self.ws.get(dev)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
+            self.ws[dev] = buf
+        return buf
+
+    def host(self, key, nbytes):
+        import torch
+        buf = self.pinned.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 1 << 16), dtype=torch.uint8, pin_memory=True)
+            self.pinned[key] = buf
+        return buf
+
+
+_BUF = _Buffers()
+
+
+def _outcome_layout(B: int, H: int):
+    """Packed device buffer: hist (B*H f64) | shist (B*H f64) | sidx (B i64) |
+    iters (B i32) | status (B i32)."""
+    o_sh = B * H * 8
+    o_sidx = 2 * B * H * 8
+    o_it = o_sidx + B * 8
+    o_st = o_it + B * 4
+    return o_sh, o_sidx, o_it, o_st, o_st + B * 4
+
+
 def solve_device(P, S, x0, X, dt: float, config: NewtonConfig, *, stream=None):
     """Run the native solve on device tensors (x0: (B, d), X: (B, N, d), fp64, CUDA).
 
-    X is overwritten with the final iterates.  Returns device tensors
-    (hist, shist, iters, status, status_index) without synchronising.
+    X is overwritten with the final iterates.  Returns the packed device
+    outcome buffer (see _outcome_layout) without synchronising; entries of
+    hist past the iterations actually run are left unwritten.
     """
     import torch
     assert X.is_cuda and X.dtype == torch.float64 and X.is_contiguous()
     B, n, d = X.shape
     dev = X.device
     H = config.max_iters + 1
-    hist = torch.full((B, H), float("nan"), dtype=torch.float64, device=dev)
-    shist = torch.full((B, H), float("nan"), dtype=torch.float64, device=dev)
-    iters = torch.zeros(B, dtype=torch.int32, device=dev)
-    status = torch.full((B,), -1, dtype=torch.int32, device=dev)
-    sidx = torch.full((B,), -1, dtype=torch.int64, device=dev)
+    o_sh, o_sidx, o_it, o_st, total = _outcome_layout(B, H)
+    out = torch.empty(total, dtype=torch.uint8, device=dev)
+    base = out.data_ptr()
     cfg = N.make_cfg(config.max_iters, config.residual_tol, config.step_tol,
                      config.abort_on_nonfinite)
     L = N.lib()
     ws_bytes = L.odx_solve_workspace_bytes(P, S, B, n, cfg)
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    ws = _BUF.workspace(dev, ws_bytes)
     st = stream if stream is not None else N.stream_handle(dev)
-    N.check(L.odx_solve(P, S, N.ptr(x0), N.ptr(X), B, n, float(dt), cfg, N.ptr(hist),
-                        N.ptr(shist), N.ptr(iters), N.ptr(status), N.ptr(sidx), N.ptr(ws),
-                        ws_bytes, st))
+    N.check(L.odx_solve(P, S, N.ptr(x0), N.ptr(X), B, n, float(dt), cfg, base, base + o_sh,
+                        base + o_it, base + o_st, base + o_sidx, N.ptr(ws), ws.numel(), st))
+    return out
+
+
+def _unpack_outcome(out_host: np.ndarray, B: int, H: int):
+    o_sh, o_sidx, o_it, o_st, total = _outcome_layout(B, H)
+    raw = out_host[:total]
+    hist = raw[:o_sh].view(np.float64).reshape(B, H).copy()
+    shist = raw[o_sh:o_sidx].view(np.float64).reshape(B, H).copy()
+    sidx = raw[o_sidx:o_it].view(np.int64).copy()
+    iters = raw[o_it:o_st].view(np.int32).copy()
+    status = raw[o_st:total].view(np.int32).copy()
+    cols = np.arange(H)[None, :]
+    reached = cols <= np.where(status == N.ST_SINGULAR, iters - 1, iters)[:, None]
+    hist[~reached] = np.nan
+    shist[~reached] = np.nan
     return hist, shist, iters, status, sidx
+
+
+def _to_device(arr, dev, key):
+    """Host numpy -> device through a pinned staging buffer (one async H2D)."""
+    import torch
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    stage = _BUF.host(key, a.nbytes)
+    view = stage[: a.nbytes].numpy().view(np.float64).reshape(a.shape)
+    np.copyto(view, a)
+    t = torch.empty(a.shape, dtype=torch.float64, device=dev)
+    t.copy_(stage[: a.nbytes].view(torch.float64).view(a.shape), non_blocking=True)
+    return t
+
+
+def _fetch(dev_tensor, key):
+    """Device -> host numpy through pinned staging; caller synchronises."""
+    import torch
+    nbytes = dev_tensor.numel() * dev_tensor.element_size()
+    stage = _BUF.host(key, nbytes)
+    dst = stage[:nbytes].view(dev_tensor.dtype).view(dev_tensor.shape)
+    dst.copy_(dev_tensor, non_blocking=True)
+    return dst
 
 
 def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones",
@@ -263,21 +337,25 @@ def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones
     if _is_torch(start.states):
         X = start.states.detach().to(device=dev, dtype=torch.float64).clone().contiguous()
     else:
-        X = torch.from_numpy(np.ascontiguousarray(start.states, np.float64)).to(dev)
+        X = _to_device(start.states, dev, ("X", dev))
     X = X.reshape(1, n, problem.dim)
-    x0 = torch.from_numpy(np.ascontiguousarray(problem.x0, np.float64)).to(dev).reshape(1, -1)
-    hist, shist, iters, status, sidx = solve_device(P, S, x0, X, dt, config)
-    small = torch.cat([iters.to(torch.int64), status.to(torch.int64), sidx]).cpu().tolist()
-    it_run, st, idx = int(small[0]), int(small[1]), int(small[2])
+    x0 = _to_device(problem.x0.reshape(1, -1), dev, ("x0", dev))
+    H = config.max_iters + 1
+    out = solve_device(P, S, x0, X, dt, config)
+    out_h = _fetch(out, ("out", dev))
+    states_h = None if output == "torch" else _fetch(X[0], ("Xo", dev))
+    torch.cuda.current_stream(dev).synchronize()
+    hist, shist, iters, status, sidx = _unpack_outcome(out_h.numpy(), 1, H)
+    it_run, st, idx = int(iters[0]), int(status[0]), int(sidx[0])
     if st == N.ST_SINGULAR:
         raise SingularDiagonalBlockError(idx)
     if st == N.ST_NONFINITE:
         raise NonFiniteError(idx)
     if st < 0:
         raise RuntimeError("device solve did not report a status")
-    h = hist[0, : it_run + 1].cpu().numpy()
-    sh = shist[0, : it_run + 1].cpu().numpy()
-    states = X[0] if output == "torch" else X[0].cpu().numpy()
+    h = hist[0, : it_run + 1]
+    sh = shist[0, : it_run + 1]
+    states = X[0] if output == "torch" else states_h.numpy().copy()
     wall = time.perf_counter() - t_begin
     traj = Trajectory(problem.x0.copy(), states, dt, n)
     rec = config.record_residuals
@@ -305,8 +383,8 @@ def solve_batch(problem: OdeProblem, stepper: StepperIncrement, dt: float, x0s, 
     n = n_steps_for(problem, dt)
     dev = _device(device)
     t_begin = time.perf_counter()
-    x0t = (x0s.detach().to(dev, torch.float64) if _is_torch(x0s)
-           else torch.from_numpy(np.ascontiguousarray(x0s, np.float64)).to(dev)).contiguous()
+    x0t = (x0s.detach().to(dev, torch.float64).contiguous() if _is_torch(x0s)
+           else _to_device(np.asarray(x0s), dev, ("x0", dev)))
     B, d = x0t.shape
     if d != problem.dim:
         raise ValueError(f"x0s has dim {d}, expected {problem.dim}")
@@ -314,19 +392,22 @@ def solve_batch(problem: OdeProblem, stepper: StepperIncrement, dt: float, x0s, 
         X = x0t[:, None, :].expand(B, n, d).contiguous()
     elif isinstance(guess, str):
         g = initial_guess(guess, problem, n).states
-        X = torch.from_numpy(g).to(dev)[None].expand(B, n, d).contiguous()
+        X = _to_device(g, dev, ("X", dev))[None].expand(B, n, d).contiguous()
     elif _is_torch(guess):
         X = guess.detach().to(dev, torch.float64).clone().contiguous()
     else:
-        X = torch.from_numpy(np.array(guess, np.float64)).to(dev).contiguous()
+        X = _to_device(np.asarray(guess), dev, ("X", dev))
     if tuple(X.shape) != (B, n, d):
         raise ValueError(f"guess has shape {tuple(X.shape)}, expected {(B, n, d)}")
-    hist, shist, iters, status, sidx = solve_device(P, S, x0t, X, dt, config)
-    torch.cuda.synchronize(dev)
+    H = config.max_iters + 1
+    out = solve_device(P, S, x0t, X, dt, config)
+    out_h = _fetch(out, ("out", dev))
+    states_h = None if output == "torch" else _fetch(X, ("Xo", dev))
+    torch.cuda.current_stream(dev).synchronize()
+    hist, shist, iters, status, sidx = _unpack_outcome(out_h.numpy(), B, H)
     rep = BatchSolveReport(
-        states=X if output == "torch" else X.cpu().numpy(),
-        residual_history=hist.cpu().numpy(), scaled_residual_history=shist.cpu().numpy(),
-        iterations_run=iters.cpu().numpy(), status=status.cpu().numpy(),
-        status_index=sidx.cpu().numpy(), wall_time=0.0)
+        states=X if output == "torch" else states_h.numpy().copy(),
+        residual_history=hist, scaled_residual_history=shist, iterations_run=iters,
+        status=status, status_index=sidx, wall_time=0.0)
     rep.wall_time = time.perf_counter() - t_begin
     return rep
