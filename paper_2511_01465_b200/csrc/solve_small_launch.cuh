@@ -136,6 +136,8 @@ int launch_ws(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
     if (per_sm < 1) return fail(ODX_ECUDA, "persistent kernel cannot be resident");
     long long grid = (long long)per_sm * num_sms();
     if (grid > lay.ntiles) grid = lay.ntiles;
+    if (getenv("ODX_VERBOSE"))
+        fprintf(stderr, "launch_ws: T=%d smem=%zu per_sm=%d grid=%lld\n", W::T, smem, per_sm, grid);
     void* args[] = {&wp};
     ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(W::NT), args,
                                          smem, st));

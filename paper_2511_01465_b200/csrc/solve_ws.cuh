@@ -51,8 +51,18 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ __forceinline__ unsigned long long gtime() { return 0; }
 #endif
 
-template <int D>
+// A tile's look-back record: aggregate (F, c) then inclusive prefix, one
+// self-validating chunk per double.  The chunk count is padded to an odd number
+// so that, with an odd number of tiles per lane (LBK), the lanes' shared-memory
+// reads of a staged look-back window fall on distinct banks.
+template <int D, bool PAD = ((D * D + 2 * D) % 2 == 0)>
 struct LbRecord {
+    Chunk agg[D * D + D];
+    Chunk incl[D];
+    Chunk pad;
+};
+template <int D>
+struct LbRecord<D, false> {
     Chunk agg[D * D + D];
     Chunk incl[D];
 };
@@ -271,6 +281,151 @@ done:
     }
 }
 
+// Wide decoupled look-back, one L2 round trip per round: each lane covers LBK
+// consecutive tiles (a round examines 32*LBK tiles); all their record chunks
+// ({value, tag}, 16 B) are staged into the lane's shared-memory area with one
+// batch of cp.async, then validated from smem (self-validating tags) — tiles
+// not yet published are re-fetched.  Returns the exclusive prefix state (lane 0).
+constexpr int LBK = 5;  // odd: see LbRecord
+
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+template <int D>
+__device__ __forceinline__ void lookback_wide1(long long t, unsigned long long tagA,
+                                               unsigned long long tagI, const LbRecord<D>* recs,
+                                               Chunk* area /* [32*LBK][E + D] per warp */,
+                                               uint64_t* lbbar, uint32_t& lbph,
+                                               double* z, int lane, long long* stats = nullptr) {
+    constexpr int E = D * D + D;
+    constexpr int RCP = (int)(sizeof(LbRecord<D>) / sizeof(Chunk));  // padded record
+    constexpr int WT = 32 * LBK;  // tiles per round
+    long long n_rounds = 0, n_spins = 0, t_copy = 0, t_red = 0, t_tma = 0;
+    Elem<D> R;
+    bool R_has = false;
+    long long pos = t - 1;  // round covers tiles pos, pos-1, ..., pos-WT+1
+    while (true) {
+        // lane owns round-relative tiles j = lane*LBK + k (k = 0..LBK-1)
+        const long long hi = pos - (long long)lane * LBK;
+        const int nreal = hi < 0 ? 0 : (hi + 1 < LBK ? (int)(hi + 1) : LBK);
+        unsigned valid = 0, incl = 0;  // this lane's per-tile bits
+        const unsigned need = (1u << nreal) - 1u;
+        int spins = 0;
+        long long tc0 = (long long)gtime();
+        // The round's records are contiguous: one TMA bulk copy (off the LSU
+        // path the compute warps keep busy) stages them; lane l's tiles sit at
+        // an odd record stride, so its reads below hit distinct banks.
+        const long long nround = pos + 1 < WT ? pos + 1 : WT;
+        const long long lo = pos - nround + 1;
+        const Chunk* my = area + (hi - lo) * RCP;  // this lane's newest tile
+        while (true) {
+            if (lane == 0) {
+                const uint32_t bytes = (uint32_t)(nround * sizeof(LbRecord<D>));
+                fence_proxy_async_smem();  // prior generic reads of the area
+                mbar_arrive_expect_tx(lbbar, bytes);
+                tma_load_1d(area, &recs[lo], bytes, lbbar);
+            }
+            mbar_wait(lbbar, lbph);
+            lbph ^= 1u;
+            if (n_spins == 0 && spins == 0) t_tma += (long long)gtime() - tc0;
+
+#pragma unroll
+            for (int k = 0; k < LBK; k++) {
+                if (k < nreal && !((valid >> k) & 1u)) {
+                    const Chunk* a = my - k * RCP;
+                    bool iv = true, av = true;
+#pragma unroll
+                    for (int c = 0; c < D; c++) iv &= (a[E + c].tag == tagI);
+#pragma unroll
+                    for (int c = 0; c < E; c++) av &= (a[c].tag == tagA);
+                    if (iv) {
+                        valid |= 1u << k;
+                        incl |= 1u << k;
+                    } else if (av) {
+                        valid |= 1u << k;
+                    }
+                }
+            }
+            if (__all_sync(FULL, (valid & need) == need)) break;
+            if (++spins > 16) __nanosleep(16);
+        }
+        n_rounds++;
+        n_spins += spins;
+        long long tc1 = (long long)gtime();
+        t_copy += tc1 - tc0;
+        // newest inclusive prefix in this lane's range, or the start sentinel
+        const int kstop = incl ? (__ffs(incl) - 1) : nreal;
+        Elem<D> acc;
+        bool acc_has = false;
+#pragma unroll
+        for (int k = 0; k < LBK; k++) {
+            if (k < kstop) {
+                Elem<D> e;
+                const Chunk* a = my - k * RCP;
+#pragma unroll
+                for (int c = 0; c < D * D; c++) e.F[c] = a[c].v;
+#pragma unroll
+                for (int c = 0; c < D; c++) e.c[c] = a[D * D + c].v;
+                if (acc_has)
+                    compose<D>(e, acc, acc);
+                else {
+                    acc = e;
+                    acc_has = true;
+                }
+            }
+        }
+        const bool found = kstop < LBK;
+        if (found) {
+            Elem<D> e;
+#pragma unroll
+            for (int c = 0; c < D * D; c++) e.F[c] = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; c++)
+                e.c[c] = (kstop < nreal) ? my[E + c - kstop * RCP].v : 0.0;
+            if (acc_has)
+                compose<D>(e, acc, acc);
+            else {
+                acc = e;
+                acc_has = true;
+            }
+        }
+        __syncwarp();  // the area is refilled in the next round
+        const unsigned m = __ballot_sync(FULL, found);
+        const int first = m ? (__ffs(m) - 1) : 32;
+        bool has = lane <= first && acc_has;
+        warp_reduce_latest_first<D>(acc, has, lane);
+        if (lane == 0 && has) {
+            if (R_has)
+                compose<D>(acc, R, R);
+            else {
+                R = acc;
+                R_has = true;
+            }
+        }
+        t_red += (long long)gtime() - tc1;
+        if (first < 32) {
+            if (stats && lane == 0) {
+                stats[0] = n_rounds;
+                stats[1] = t_tma;
+                stats[2] = t - (pos - (long long)first * LBK);
+                stats[3] = t_copy;
+                stats[4] = t_red;
+            }
+            break;
+        }
+        pos -= WT;
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < D; k++) z[k] = R.c[k];
+    }
+}
+
 template <class P, int KIND, int S, int NCW, int ITEMS>
 struct WsEngine {
     static constexpr int D = P::D;
@@ -283,7 +438,6 @@ struct WsEngine {
 
     struct Shared {
         double xr[2][T * D];  // tile rows; first member => 16-byte aligned TMA target
-        double xo[2][T * D];  // X + dx staging for the TMA bulk store
         double xh[2][D];      // halo: the state before the tile's first step
         double els[2][NCT * EST];
         double tin[2][NCT * AGS];
@@ -296,8 +450,10 @@ struct WsEngine {
         int wexhas[2][NCW];
         long long tile[2];
         uint64_t mbar[2];
+        uint64_t lbbar;  // control warp: look-back bulk copies
         double redd[3][NCW];
         unsigned long long redb[NCW];
+        LbRecord<D> lb_area[32 * LBK];  // control-warp look-back staging
     };
 };
 
@@ -326,6 +482,7 @@ persistent_ws_kernel(const WsParams wp) {
     if (tid == 0) {
         mbar_init(&sm.mbar[0], 2);  // TMA (expect_tx) + cp.async halo arrival
         mbar_init(&sm.mbar[1], 2);
+        mbar_init(&sm.lbbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -335,6 +492,7 @@ persistent_ws_kernel(const WsParams wp) {
     double step_prev = __longlong_as_double(0x7ff8000000000000ll);
     Decision dd{0, -1, -1, 0};
     uint32_t ph0 = 0, ph1 = 0;  // CW: mbarrier phase parity per buffer
+    uint32_t lbph = 0;          // CTL: look-back mbarrier phase parity
 
     for (int it = 0; it <= p.max_iters; it++) {
         const bool do_scan = it < p.max_iters;
@@ -417,7 +575,15 @@ persistent_ws_kernel(const WsParams wp) {
                     double z[D];
 #pragma unroll
                     for (int k = 0; k < D; k++) z[k] = 0.0;
-                    if (t > 0) lookback2<D, false>(t, tagA, tagI, tagG, recs, gsums, z, lane);
+                    long long lbs[5] = {0, 0, 0, 0, 0};
+                    if (t > 0) lookback_wide1<D>(t, tagA, tagI, recs, &sm.lb_area[0].agg[0], &sm.lbbar, lbph, z, lane, lbs);
+                    if (lane == 0) {
+                        TRACE(it, t, 11, (unsigned long long)lbs[0]);
+                        TRACE(it, t, 12, (unsigned long long)lbs[1]);
+                        TRACE(it, t, 13, (unsigned long long)lbs[2]);
+                        TRACE(it, t, 14, (unsigned long long)lbs[3]);
+                        TRACE(it, t, 15, (unsigned long long)lbs[4]);
+                    }
                     if (lane == 0) {
                         double incl[D];
                         apply<D>(A, z, incl);
@@ -475,6 +641,10 @@ persistent_ws_kernel(const WsParams wp) {
                     for (int k = 0; k < D; k++) e.c[k] = src[D * D + k];
                     apply<D>(e, z, z);
                 }
+                // X + dx goes straight from registers to HBM: each thread owns
+                // ITEMS*D consecutive doubles (whole 32-byte sectors), so the
+                // warp's stores are fully coalesced without a staging buffer
+                double xn[ITEMS * D];
 #pragma unroll
                 for (int i = 0; i < ITEMS; i++) {
                     const int r = tid * ITEMS + i;
@@ -491,23 +661,22 @@ persistent_ws_kernel(const WsParams wp) {
 #pragma unroll
                         for (int k = 0; k < D; k++) {
                             z[k] = dx[k];
-                            sm.xo[c][r * D + k] = xk[i][k] + dx[k];
+                            xn[i * D + k] = xk[i][k] + dx[k];
                         }
                     }
                 }
-                named_sync<BAR_CW, NCT>();
-                const long long rows = (N - base) < T ? (N - base) : T;
-                const uint32_t bytes = (uint32_t)(rows * D * 8);
-                if ((bytes & 15u) == 0) {
-                    if (tid == 0) {
-                        fence_proxy_async_smem();
-                        tma_store_1d(nxt + base * D, sm.xo[c], bytes);
-                        tma_store_commit();
-                        // the other staging buffer's store must have been read
-                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                    }
+                double* dst = nxt + (base + (long long)tid * ITEMS) * D;
+                if (base + (long long)(tid + 1) * ITEMS <= N && ((ITEMS * D) & 1) == 0 &&
+                    (reinterpret_cast<size_t>(dst) & 15) == 0) {
+#pragma unroll
+                    for (int q = 0; q < ITEMS * D; q += 2)
+                        *reinterpret_cast<double2*>(dst + q) = make_double2(xn[q], xn[q + 1]);
                 } else {
-                    for (int q = tid; q < rows * D; q += NCT) nxt[base * D + q] = sm.xo[c][q];
+#pragma unroll
+                    for (int i = 0; i < ITEMS; i++)
+                        if (base + tid * ITEMS + i < N)
+#pragma unroll
+                            for (int k = 0; k < D; k++) dst[i * D + k] = xn[i * D + k];
                 }
                 if (tid == 0) TRACE(it, base / T, 5, gtime());
             };
