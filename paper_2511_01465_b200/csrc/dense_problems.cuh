@@ -10,14 +10,28 @@
 namespace odx {
 
 // Allen-Cahn method of lines, periodic (BASELINE cfg 4): params eps, dx.
+// The dense path runs d = 64 only (dense_supported), so the periodic
+// neighbours are masks.
 struct AllenCahnRows {
-    int n;
+    static constexpr int n = 64;
     double cdiff;
     __device__ __forceinline__ AllenCahnRows(const ProbParams& q, int dim)
-        : n(dim), cdiff(q.p[0] / (q.p[1] * q.p[1])) {}
+        : cdiff(q.p[0] / (q.p[1] * q.p[1])) {
+        (void)dim;
+    }
     __device__ __forceinline__ double f(const double* x, int i) const {
         const double um = x[(i + n - 1) % n], ui = x[i], up = x[(i + 1) % n];
         return cdiff * ((um - 2.0 * ui) + up) + (ui - ui * ui * ui);
+    }
+    // Row i's entries that can be non-zero, as (column, value) pairs with the
+    // same values jac(x, i, j) returns; every other entry of row i is 0.0.
+    static constexpr int ROW_NZ = 3;
+    __device__ __forceinline__ void jac_row(const double* x, int i, int* cols, double* vals) const {
+        cols[0] = (i + n - 1) % n;
+        cols[1] = i;
+        cols[2] = (i + 1) % n;
+#pragma unroll
+        for (int q = 0; q < ROW_NZ; q++) vals[q] = jac(x, i, cols[q]);
     }
     // J[i][j] for j in [0, n)
     __device__ __forceinline__ double jac(const double* x, int i, int j) const {

@@ -26,6 +26,8 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "dense_band.cuh"
+#include "dense_lu.cuh"
 #include "dense_problems.cuh"
 #include "scan.cuh"
 #include "sm100.cuh"
@@ -69,6 +71,8 @@ struct DenseParams {
     long long* first_bad;     // ops only
     DenseState* st;           // null for ops
     int nchunks;
+    long long* flist;         // steps the band kernel hands to the warp LU
+    unsigned* fcount;         // per iteration (solve) or one slot (ops)
 };
 
 // ---- NaN-ignoring row rule over 64 entries held two per lane (_kernels.py:84-95)
@@ -222,6 +226,224 @@ dense_build_kernel(const DenseParams p, int it) {
     }
     // block reduction (only warp 0 holds rn/scn; bad is uniform per block)
     if (tid == 0) {
+        if (p.red) {
+            unsigned long long* red = p.red + 4ll * it;
+            if (rn > 0.0) atomicMax(red + 0, dbits(rn));
+            if (scn > 0.0) atomicMax(red + 1, dbits(scn));
+            if (bad != ~0ull) atomicMin(red + 3, bad);
+        }
+        if (p.first_bad && bad != ~0ull) atomicMin(p.first_bad, (long long)bad);
+    }
+}
+
+// =========================================================================
+// K1 (sparse-aware LU): one warp per step, see dense_lu.cuh
+// =========================================================================
+template <class DP, bool LIST>
+__global__ void __launch_bounds__(LU_WARPS * 32)
+dense_lu_build_kernel(const DenseParams p, int it) {
+    if (p.st && p.st->stopped) return;
+    extern __shared__ __align__(16) double dsm[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    LuWarpSmem& W = reinterpret_cast<LuWarpSmem*>(dsm)[w];
+    const DP prob(p.prob, DN);
+    const double* Xc = (p.st && p.st->cur) ? p.Xalt : p.X;
+    const long long N = p.N;
+    double rn = 0.0, scn = 0.0;
+    unsigned long long bad = ~0ull;
+    const long long nw = (long long)gridDim.x * LU_WARPS;
+    const long long count = LIST ? (long long)p.fcount[it] : N;
+    for (long long q = (long long)blockIdx.x * LU_WARPS + w; q < count; q += nw) {
+        const long long k = LIST ? p.flist[q] : q;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int r = lane + 32 * h;
+            W.xk[r] = Xc[k * DN + r];
+            W.xp[r] = (k == 0) ? p.x0[r] : Xc[(k - 1) * DN + r];
+        }
+        __syncwarp();
+        double hv[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int r = lane + 32 * h;
+            const double fp = prob.f(W.xp, r), fn = prob.f(W.xk, r);
+            hv[h] = W.xk[r] - W.xp[r] - p.sc.dt * (p.sc.w_prev * fp + p.sc.w_next * fn);
+            W.cs[r] = -hv[h];
+            if (p.h) p.h[k * DN + r] = hv[h];
+        }
+        rn = nan_drop_max(rn, warp_row_rule64(hv[0], hv[1]));
+        const bool with_F = (k != 0);
+        // A = I - dt w_next Jn and B = I + dt w_prev Jp: identity everywhere
+        // the Jacobian row is structurally 0 (dij -/+ dt w * 0.0 == dij), the
+        // reference's non-contracted expressions at the DP::ROW_NZ entries
+        {
+            double2* a2 = reinterpret_cast<double2*>(W.A);
+            for (int q = lane; q < LU_N * LU_LD / 2; q += 32) a2[q] = make_double2(0.0, 0.0);
+            if (with_F) {
+                double2* x2 = reinterpret_cast<double2*>(W.X);
+                for (int q = lane; q < LU_N * LU_N / 2; q += 32) x2[q] = make_double2(0.0, 0.0);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int r = lane + 32 * h;
+                W.A[r * LU_LD + r] = 1.0;
+                if (with_F) W.X[r * LU_N + r] = 1.0;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int r = lane + 32 * h;
+                int cols[DP::ROW_NZ];
+                double vals[DP::ROW_NZ];
+                prob.jac_row(W.xk, r, cols, vals);
+#pragma unroll
+                for (int q = 0; q < DP::ROW_NZ; q++) {
+                    const double dij = (r == cols[q]) ? 1.0 : 0.0;
+                    W.A[r * LU_LD + cols[q]] = __dsub_rn(dij, __dmul_rn(p.sc.dt_wnext, vals[q]));
+                }
+                if (with_F) {
+                    prob.jac_row(W.xp, r, cols, vals);
+#pragma unroll
+                    for (int q = 0; q < DP::ROW_NZ; q++) {
+                        const double dij = (r == cols[q]) ? 1.0 : 0.0;
+                        W.X[r * LU_N + cols[q]] = __dadd_rn(__dmul_rn(p.sc.dt_wprev, vals[q]), dij);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const int sk = warp_lu_factor(W, lane);
+        double* Fk = p.F + k * DN * DN;
+        if (sk >= 0) {
+            if ((unsigned long long)k < bad) bad = (unsigned long long)k;
+            for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+            p.c[k * DN + lane] = 0.0;
+            p.c[k * DN + lane + 32] = 0.0;
+        } else {
+            warp_lu_masks(W, lane);
+            warp_lu_solve3(W, lane, with_F);
+            __syncwarp();
+            if (with_F) {
+                for (int r = 0; r < DN; r++) {
+                    Fk[r * DN + lane] = W.X[r * LU_N + lane];
+                    Fk[r * DN + lane + 32] = W.X[r * LU_N + lane + 32];
+                }
+            } else {
+                for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+            }
+            const double c0 = W.cs[lane], c1 = W.cs[lane + 32];
+            p.c[k * DN + lane] = c0;
+            p.c[k * DN + lane + 32] = c1;
+            scn = nan_drop_max(scn, warp_row_rule64(c0, c1));
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (p.red) {
+            unsigned long long* red = p.red + 4ll * it;
+            if (rn > 0.0) atomicMax(red + 0, dbits(rn));
+            if (scn > 0.0) atomicMax(red + 1, dbits(scn));
+            if (bad != ~0ull) atomicMin(red + 3, bad);
+        }
+        if (p.first_bad && bad != ~0ull) atomicMin(p.first_bad, (long long)bad);
+    }
+}
+
+// =========================================================================
+// K1 fast path: periodic-tridiagonal band LU, one warp per step (dense_band.cuh)
+// =========================================================================
+template <class DP>
+__global__ void __launch_bounds__(BAND_WARPS * 32)
+dense_band_build_kernel(const DenseParams p, int it) {
+    if (p.st && p.st->stopped) return;
+    __shared__ BandWarpSmem bsm[BAND_WARPS];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    BandWarpSmem& W = bsm[w];
+    const DP prob(p.prob, DN);
+    const double* Xc = (p.st && p.st->cur) ? p.Xalt : p.X;
+    const long long N = p.N;
+    double rn = 0.0, scn = 0.0;
+    unsigned long long bad = ~0ull;
+    const long long nw = (long long)gridDim.x * BAND_WARPS;
+    for (long long k = (long long)blockIdx.x * BAND_WARPS + w; k < N; k += nw) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int r = lane + 32 * h;
+            W.xk[r] = Xc[k * DN + r];
+            W.xp[r] = (k == 0) ? p.x0[r] : Xc[(k - 1) * DN + r];
+        }
+        __syncwarp();
+        double hv[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int r = lane + 32 * h;
+            const double fp = prob.f(W.xp, r), fn = prob.f(W.xk, r);
+            hv[h] = W.xk[r] - W.xp[r] - p.sc.dt * (p.sc.w_prev * fp + p.sc.w_next * fn);
+            W.c[r] = -hv[h];
+            if (p.h) p.h[k * DN + r] = hv[h];
+            // bands of A = I - dt w_next Jn and B = I + dt w_prev Jp
+            int cols[DP::ROW_NZ];
+            double vals[DP::ROW_NZ];
+            prob.jac_row(W.xk, r, cols, vals);
+            W.Al[r] = __dsub_rn(0.0, __dmul_rn(p.sc.dt_wnext, vals[0]));
+            W.Ad[r] = __dsub_rn(1.0, __dmul_rn(p.sc.dt_wnext, vals[1]));
+            W.Au[r] = __dsub_rn(0.0, __dmul_rn(p.sc.dt_wnext, vals[2]));
+            prob.jac_row(W.xp, r, cols, vals);
+            W.Bl[r] = __dadd_rn(__dmul_rn(p.sc.dt_wprev, vals[0]), 0.0);
+            W.Bd[r] = __dadd_rn(__dmul_rn(p.sc.dt_wprev, vals[1]), 1.0);
+            W.Bu[r] = __dadd_rn(__dmul_rn(p.sc.dt_wprev, vals[2]), 0.0);
+        }
+        rn = nan_drop_max(rn, warp_row_rule64(hv[0], hv[1]));
+        __syncwarp();
+        const int fr = band_factor_solve_c(W);
+        __syncwarp();
+        double* Fk = p.F + k * DN * DN;
+        bool handoff = (fr < 0);
+        if (fr > 0) {  // singular pivot fr - 1 (no row swap involved)
+            if ((unsigned long long)k < bad) bad = (unsigned long long)k;
+            for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+            p.c[k * DN + lane] = 0.0;
+            p.c[k * DN + lane + 32] = 0.0;
+        } else if (fr == 0) {
+            const double c0 = W.c[lane], c1 = W.c[lane + 32];
+            bool fin = isfinite(c0) && isfinite(c1);
+            if (k != 0) {
+#pragma unroll 1
+                for (int pass = 0; pass < 2; pass++) {
+                    const int col = lane + 32 * pass;
+                    const int cm = (col + BAND_N - 1) & (BAND_N - 1), cp = (col + 1) & (BAND_N - 1);
+                    const double bu = W.Bu[cm], bd = W.Bd[col], bl = W.Bl[cp];
+                    double x[BAND_N];
+#pragma unroll
+                    for (int r = 0; r < BAND_N; r++)
+                        x[r] = (r == col) ? bd : (r == cm) ? bu : (r == cp) ? bl : 0.0;
+                    band_solve_col(W, x);
+                    double chk = 0.0;
+#pragma unroll
+                    for (int r = 0; r < BAND_N; r++) {
+                        Fk[r * DN + col] = x[r];
+                        chk = fma(x[r], 0.0, chk);
+                    }
+                    fin = fin && !isnan(chk);
+                }
+            } else {
+                for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+            }
+            handoff = __any_sync(FULL, !fin);
+            if (!handoff) {
+                p.c[k * DN + lane] = c0;
+                p.c[k * DN + lane + 32] = c1;
+                scn = nan_drop_max(scn, warp_row_rule64(c0, c1));
+            }
+        }
+        if (handoff && lane == 0) {
+            const unsigned slot = atomicAdd(p.fcount + it, 1u);
+            p.flist[slot] = k;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
         if (p.red) {
             unsigned long long* red = p.red + 4ll * it;
             if (rn > 0.0) atomicMax(red + 0, dbits(rn));
@@ -483,9 +705,10 @@ static bool is_dense(const odx_problem* P, const odx_stepper* S) {
 int dense_supported(const odx_problem* P, const odx_stepper* S) { return is_dense(P, S) ? 1 : 0; }
 
 static size_t build_smem() { return (size_t)(DN * GJLD + 3 * DN) * sizeof(double); }
+static size_t lu_smem() { return LU_WARPS * sizeof(LuWarpSmem); }
 
 struct DenseLayout {
-    size_t total, F, c, aggP, aggy, red, st, Xalt;
+    size_t total, F, c, aggP, aggy, red, st, Xalt, flist, fcount;
     DenseLayout(long long N, int C, int max_iters, bool with_X) {
         size_t off = 0;
         auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
@@ -496,6 +719,8 @@ struct DenseLayout {
         red = at(4 * ((size_t)max_iters + 1) * 8);
         st = at(sizeof(DenseState));
         Xalt = with_X ? at((size_t)N * DN * 8) : 0;
+        flist = at((size_t)N * 8);
+        fcount = at(((size_t)max_iters + 1) * 4);
         total = off + 256;
     }
 };
@@ -543,24 +768,30 @@ int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, voi
     p.red = reinterpret_cast<unsigned long long*>(base + lay.red);
     p.st = reinterpret_cast<DenseState*>(base + lay.st);
     p.nchunks = (int)((sp.N < C) ? sp.N : C);
+    p.flist = reinterpret_cast<long long*>(base + lay.flist);
+    p.fcount = reinterpret_cast<unsigned*>(base + lay.fcount);
     const int H = sp.max_iters + 1;
     dense_init_kernel<<<(H + 127) / 128, 128, 0, st>>>(p.st, p.red, H);
-    auto k1 = dense_build_kernel<AllenCahnRows>;
-    int rc = set_smem(k1, build_smem());
+    ODX_CUDA(cudaMemsetAsync(p.fcount, 0, (size_t)H * 4, st));
+    auto kb = dense_band_build_kernel<AllenCahnRows>;
+    auto k1 = dense_lu_build_kernel<AllenCahnRows, true>;
+    int rc = set_smem(k1, lu_smem());
     if (rc) return rc;
     rc = set_smem(dense_agg_kernel, sizeof(AggSmem));
     if (rc) return rc;
     rc = set_smem(dense_fixup_kernel, sizeof(FixSmem));
     if (rc) return rc;
     int per_sm = 0;
-    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, DTHREADS, build_smem()));
-    long long g1 = (long long)(per_sm < 1 ? 1 : per_sm) * num_sms();
-    if (g1 > sp.N) g1 = sp.N;
-    int launches = 1;
+    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BAND_WARPS * 32, 0));
+    long long gb = (long long)(per_sm < 1 ? 1 : per_sm) * num_sms();
+    if (gb > (sp.N + BAND_WARPS - 1) / BAND_WARPS) gb = (sp.N + BAND_WARPS - 1) / BAND_WARPS;
+    const long long g1 = num_sms();  // list-driven exact LU (normally no work)
+    int launches = 2;
     for (int it = 0; it <= sp.max_iters; it++) {
-        k1<<<(unsigned)g1, DTHREADS, build_smem(), st>>>(p, it);
+        kb<<<(unsigned)gb, BAND_WARPS * 32, 0, st>>>(p, it);
+        k1<<<(unsigned)g1, LU_WARPS * 32, lu_smem(), st>>>(p, it);
         dense_decide_kernel<<<1, 1, 0, st>>>(p, it);
-        launches += 2;
+        launches += 3;
         if (it < sp.max_iters) {
             dense_agg_kernel<<<p.nchunks, DTHREADS, sizeof(AggSmem), st>>>(p);
             dense_fixup_kernel<<<p.nchunks, DTHREADS, sizeof(FixSmem), st>>>(p, it);
@@ -595,16 +826,25 @@ int dense_build_op(const odx_problem* P, const odx_stepper* S, const StepCoefs& 
     p.first_bad = first_bad;
     set_i64_dense<<<1, 1, 0, st>>>(first_bad, LLONG_MAX);
     if (N > 0) {
-        auto k1 = dense_build_kernel<AllenCahnRows>;
-        int rc = set_smem(k1, build_smem());
+        auto kb = dense_band_build_kernel<AllenCahnRows>;
+        auto k1 = dense_lu_build_kernel<AllenCahnRows, true>;
+        int rc = set_smem(k1, lu_smem());
         if (rc) return rc;
-        long long g1 = 3LL * num_sms();
-        if (g1 > N) g1 = N;
-        k1<<<(unsigned)g1, DTHREADS, build_smem(), st>>>(p, 0);
+        // hand-off list: stream-ordered scratch (ops carry no workspace)
+        void* scratch = nullptr;
+        ODX_CUDA(cudaMallocAsync(&scratch, (size_t)N * 8 + 256, st));
+        p.flist = reinterpret_cast<long long*>(scratch);
+        p.fcount = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(scratch) + align_up((size_t)N * 8, 256));
+        ODX_CUDA(cudaMemsetAsync(p.fcount, 0, 4, st));
+        long long gb = 4LL * num_sms();
+        if (gb > (N + BAND_WARPS - 1) / BAND_WARPS) gb = (N + BAND_WARPS - 1) / BAND_WARPS;
+        kb<<<(unsigned)gb, BAND_WARPS * 32, 0, st>>>(p, 0);
+        k1<<<(unsigned)num_sms(), LU_WARPS * 32, lu_smem(), st>>>(p, 0);
+        ODX_CUDA(cudaFreeAsync(scratch, st));
     }
     finalize_bad_dense<<<1, 1, 0, st>>>(first_bad);
     ODX_CUDA(cudaGetLastError());
-    count_launch(N > 0 ? 3 : 2);
+    count_launch(N > 0 ? 4 : 2);
     return ODX_OK;
 }
 

@@ -359,6 +359,31 @@ def test_dense_build_op_vs_golden(pkg, golden_kernels):
             scaled_close(got.cpu().numpy(), ref, TOL, key)
 
 
+def test_dense_build_op_pivoting_and_nonfinite(pkg, oracle):
+    """The warp LU against the oracle where partial pivoting swaps rows
+    (dt < 0 makes |A_kk| < |A_k+1,k|; u near 2.52 makes A_kk ~ 0) and where
+    NaN / inf states poison the elimination (full-block updates)."""
+    from paper_2511_01465_b200 import kernels as K
+    prob = pkg.allen_cahn()
+    pid, params = prob.device
+    rng = np.random.default_rng(11)
+    n = 96
+    X = rng.uniform(-3.0, 3.0, size=(n, 64))
+    X[7, :] = 2.5177
+    X[9, 5] = np.nan
+    X[20, 63] = np.inf
+    X[33, :] = 0.0
+    x0 = rng.uniform(-1.0, 1.0, size=64)
+    for stname, (wp, wn) in (("backward_euler", (0.0, 1.0)), ("trapezoidal", (0.5, 0.5))):
+        for dt in (-0.01, 0.003):
+            st = pkg.get_stepper(stname, prob)
+            Fe, ce, h, bad = K.build_implicit(prob, st, dev(x0), dev(X), dt)
+            rF, rc, rh, rbad = oracle.build_implicit(pid, params, wp, wn, x0, X, dt)
+            assert bad == rbad, (stname, dt, bad, rbad)
+            for got, ref, what in ((h, rh, "h"), (ce, rc, "c"), (Fe, rF, "F")):
+                scaled_close(got.cpu().numpy(), ref, TOL, f"{stname} dt={dt} {what}")
+
+
 def test_cfg4_small_vs_golden(pkg, golden_baseline):
     from paper_2511_01465_b200.configs import CONFIGS
     g = golden_baseline
