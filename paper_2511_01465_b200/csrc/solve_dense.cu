@@ -36,8 +36,6 @@
 namespace odx {
 
 constexpr int DN = 64;            // dense state dimension
-constexpr int GJW = 2 * DN + 1;   // [A | B | -h]
-constexpr int GJLD = GJW + 1;     // 130
 constexpr int FLD = 68;           // padded leading dim of GEMM operands (conflict-free DMMA)
 constexpr int DTHREADS = 256;
 
@@ -67,10 +65,12 @@ struct DenseParams {
     double* h;   // N x 64 (ops only) or null
     double* aggP;  // nchunks x 64 x 64
     double* aggy;  // nchunks x 64
+    double* zin;   // nchunks x 64: state before each chunk
     unsigned long long* red;  // 4 per iteration: rn, sc, step, bad
     long long* first_bad;     // ops only
     DenseState* st;           // null for ops
     int nchunks;
+    int fld;                  // row stride of F in memory: FLD (solve workspace) or DN (ops)
     long long* flist;         // steps the band kernel hands to the warp LU
     unsigned* fcount;         // per iteration (solve) or one slot (ops)
 };
@@ -96,144 +96,6 @@ __device__ __forceinline__ double warp_row_rule64(double a, double b) {
 __device__ __forceinline__ int chunk_begin(long long N, int C, int c) {
     const long long base = N / C, rem = N % C;
     return (int)(c * base + (c < rem ? c : rem));
-}
-
-// =========================================================================
-// K1: per-step Gauss-Jordan build
-// =========================================================================
-template <class DP>
-__global__ void __launch_bounds__(DTHREADS)
-dense_build_kernel(const DenseParams p, int it) {
-    if (p.st && p.st->stopped) return;
-    extern __shared__ __align__(16) double dsm[];
-    double* aug = dsm;                 // 64 x GJLD
-    double* xp = aug + DN * GJLD;      // 64
-    double* xk = xp + DN;              // 64
-    double* mult = xk + DN;            // 64
-    __shared__ int s_piv, s_sing;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const DP prob(p.prob, DN);
-    const double* Xc = (p.st && p.st->cur) ? p.Xalt : p.X;
-    const long long N = p.N;
-    double rn = 0.0, scn = 0.0;
-    unsigned long long bad = ~0ull;
-
-    for (long long k = blockIdx.x; k < N; k += gridDim.x) {
-        if (tid < DN) {
-            xk[tid] = Xc[k * DN + tid];
-            xp[tid] = (k == 0) ? p.x0[tid] : Xc[(k - 1) * DN + tid];
-        }
-        __syncthreads();
-        double hv = 0.0;
-        if (tid < DN) {
-            const double fp = prob.f(xp, tid), fn = prob.f(xk, tid);
-            hv = xk[tid] - xp[tid] - p.sc.dt * (p.sc.w_prev * fp + p.sc.w_next * fn);
-            aug[tid * GJLD + 2 * DN] = -hv;
-            if (p.h) p.h[k * DN + tid] = hv;
-        }
-        for (int q = tid; q < DN * DN; q += DTHREADS) {
-            const int i = q / DN, j = q % DN;
-            const double dij = (i == j) ? 1.0 : 0.0;
-            aug[i * GJLD + j] = __dsub_rn(dij, __dmul_rn(p.sc.dt_wnext, prob.jac(xk, i, j)));
-            aug[i * GJLD + DN + j] = __dadd_rn(__dmul_rn(p.sc.dt_wprev, prob.jac(xp, i, j)), dij);
-        }
-        __syncthreads();
-        if (w == 0) {
-            const double a = -aug[lane * GJLD + 2 * DN], b = -aug[(lane + 32) * GJLD + 2 * DN];
-            rn = nan_drop_max(rn, warp_row_rule64(a, b));
-        }
-        // ---- Gauss-Jordan with partial pivoting ----------------------------
-        bool singular = false;
-        for (int pc = 0; pc < DN; pc++) {
-            if (w == 0) {
-                // reference pivot rule (_kernels.py:36-45): start from row pc,
-                // a later row wins only if strictly larger; NaN never wins
-                const double d0 = fabs(aug[pc * GJLD + pc]);
-                int bi = pc;
-                double bv = d0;
-                if (!isnan(d0)) {
-                    for (int r = pc + 1 + lane; r < DN; r += 32) {
-                        const double v = fabs(aug[r * GJLD + pc]);
-                        if (v > bv) {  // first max within the lane's rows
-                            bv = v;
-                            bi = r;
-                        }
-                    }
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
-                        const double ov = __shfl_xor_sync(FULL, bv, off);
-                        const int oi = __shfl_xor_sync(FULL, bi, off);
-                        if (ov > bv || (ov == bv && oi < bi)) {
-                            bv = ov;
-                            bi = oi;
-                        }
-                    }
-                }
-                if (lane == 0) {
-                    s_piv = bi;
-                    s_sing = (bv < 1e-300) ? 1 : 0;
-                }
-            }
-            __syncthreads();
-            if (s_sing) {
-                singular = true;
-                break;
-            }
-            const int pv = s_piv;
-            if (pv != pc) {
-                for (int j = tid; j < GJW; j += DTHREADS) {
-                    const double t = aug[pc * GJLD + j];
-                    aug[pc * GJLD + j] = aug[pv * GJLD + j];
-                    aug[pv * GJLD + j] = t;
-                }
-                __syncthreads();
-            }
-            if (tid < DN) {
-                const double inv = 1.0 / aug[pc * GJLD + pc];
-                mult[tid] = (tid == pc) ? 0.0 : aug[tid * GJLD + pc] * inv;
-            }
-            __syncthreads();
-            const int width = GJW - pc - 1;
-            for (int q = tid; q < DN * width; q += DTHREADS) {
-                const int i = q / width, j = pc + 1 + q % width;
-                if (i == pc) continue;
-                const double m = mult[i];
-                if (j < DN)
-                    aug[i * GJLD + j] = __dsub_rn(aug[i * GJLD + j], __dmul_rn(m, aug[pc * GJLD + j]));
-                else
-                    aug[i * GJLD + j] = aug[i * GJLD + j] - m * aug[pc * GJLD + j];
-            }
-            __syncthreads();
-        }
-        // ---- results: F = A^{-1} B (0 at step 0), c = A^{-1}(-h) -------------
-        if (singular) {
-            if ((unsigned long long)k < bad) bad = (unsigned long long)k;
-            for (int q = tid; q < DN * DN; q += DTHREADS) p.F[k * DN * DN + q] = 0.0;
-            if (tid < DN) p.c[k * DN + tid] = 0.0;
-        } else {
-            for (int q = tid; q < DN * DN; q += DTHREADS) {
-                const int i = q / DN, j = q % DN;
-                p.F[k * DN * DN + q] = (k == 0) ? 0.0 : aug[i * GJLD + DN + j] / aug[i * GJLD + i];
-            }
-            if (tid < DN) p.c[k * DN + tid] = aug[tid * GJLD + 2 * DN] / aug[tid * GJLD + tid];
-            if (w == 0) {
-                const double a = aug[lane * GJLD + 2 * DN] / aug[lane * GJLD + lane];
-                const double b = aug[(lane + 32) * GJLD + 2 * DN] / aug[(lane + 32) * GJLD + lane + 32];
-                scn = nan_drop_max(scn, warp_row_rule64(a, b));
-            }
-        }
-        __syncthreads();
-    }
-    // block reduction (only warp 0 holds rn/scn; bad is uniform per block)
-    if (tid == 0) {
-        if (p.red) {
-            unsigned long long* red = p.red + 4ll * it;
-            if (rn > 0.0) atomicMax(red + 0, dbits(rn));
-            if (scn > 0.0) atomicMax(red + 1, dbits(scn));
-            if (bad != ~0ull) atomicMin(red + 3, bad);
-        }
-        if (p.first_bad && bad != ~0ull) atomicMin(p.first_bad, (long long)bad);
-    }
 }
 
 // =========================================================================
@@ -314,10 +176,10 @@ dense_lu_build_kernel(const DenseParams p, int it) {
         }
         __syncwarp();
         const int sk = warp_lu_factor(W, lane);
-        double* Fk = p.F + k * DN * DN;
+        double* Fk = p.F + k * DN * p.fld;
         if (sk >= 0) {
             if ((unsigned long long)k < bad) bad = (unsigned long long)k;
-            for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+            for (int q = lane; q < DN * DN; q += 32) Fk[(q >> 6) * p.fld + (q & 63)] = 0.0;
             p.c[k * DN + lane] = 0.0;
             p.c[k * DN + lane + 32] = 0.0;
         } else {
@@ -326,11 +188,11 @@ dense_lu_build_kernel(const DenseParams p, int it) {
             __syncwarp();
             if (with_F) {
                 for (int r = 0; r < DN; r++) {
-                    Fk[r * DN + lane] = W.X[r * LU_N + lane];
-                    Fk[r * DN + lane + 32] = W.X[r * LU_N + lane + 32];
+                    Fk[r * p.fld + lane] = W.X[r * LU_N + lane];
+                    Fk[r * p.fld + lane + 32] = W.X[r * LU_N + lane + 32];
                 }
             } else {
-                for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+                for (int q = lane; q < DN * DN; q += 32) Fk[(q >> 6) * p.fld + (q & 63)] = 0.0;
             }
             const double c0 = W.cs[lane], c1 = W.cs[lane + 32];
             p.c[k * DN + lane] = c0;
@@ -398,11 +260,11 @@ dense_band_build_kernel(const DenseParams p, int it) {
         __syncwarp();
         const int fr = band_factor_solve_c(W);
         __syncwarp();
-        double* Fk = p.F + k * DN * DN;
+        double* Fk = p.F + k * DN * p.fld;
         bool handoff = (fr < 0);
         if (fr > 0) {  // singular pivot fr - 1 (no row swap involved)
             if ((unsigned long long)k < bad) bad = (unsigned long long)k;
-            for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+            for (int q = lane; q < DN * DN; q += 32) Fk[(q >> 6) * p.fld + (q & 63)] = 0.0;
             p.c[k * DN + lane] = 0.0;
             p.c[k * DN + lane + 32] = 0.0;
         } else if (fr == 0) {
@@ -422,13 +284,13 @@ dense_band_build_kernel(const DenseParams p, int it) {
                     double chk = 0.0;
 #pragma unroll
                     for (int r = 0; r < BAND_N; r++) {
-                        Fk[r * DN + col] = x[r];
+                        Fk[r * p.fld + col] = x[r];
                         chk = fma(x[r], 0.0, chk);
                     }
                     fin = fin && !isnan(chk);
                 }
             } else {
-                for (int q = lane; q < DN * DN; q += 32) Fk[q] = 0.0;
+                for (int q = lane; q < DN * DN; q += 32) Fk[(q >> 6) * p.fld + (q & 63)] = 0.0;
             }
             handoff = __any_sync(FULL, !fin);
             if (!handoff) {
@@ -488,9 +350,9 @@ __global__ void dense_decide_kernel(const DenseParams p, int it) {
 // DMMA 64x64x64: C = A * B, operands row-major with leading dim FLD, 8 warps
 // (warp w computes rows 8w..8w+7, all 64 columns).
 // =========================================================================
-__device__ __forceinline__ void gemm64_dmma(const double* A, const double* B, double* C) {
+// acc = A B for this warp's 8 rows (A, B row-major ld FLD in smem), fp64 DMMA
+__device__ __forceinline__ void gemm64_dmma_acc(const double* A, const double* B, double (&acc)[8][2]) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    double acc[8][2];
 #pragma unroll
     for (int n = 0; n < 8; n++) acc[n][0] = acc[n][1] = 0.0;
     const int r0 = w * 8;
@@ -506,6 +368,10 @@ __device__ __forceinline__ void gemm64_dmma(const double* A, const double* B, do
                 : "d"(a), "d"(b));
         }
     }
+}
+__device__ __forceinline__ void gemm64_store(double* C, const double (&acc)[8][2]) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int r0 = w * 8;
 #pragma unroll
     for (int n = 0; n < 8; n++) {
         C[(r0 + g) * FLD + n * 8 + 2 * t] = acc[n][0];
@@ -526,16 +392,23 @@ __device__ __forceinline__ void matvec64(const double* M, const double* y, const
 }
 
 // stage F_j (64 rows of 512 B into padded rows) and c_j through TMA
+// Called by threads 0..64 together: the 65 row copies are issued in
+// parallel (one thread issuing them all serialises ~65 TMA requests).
+// Thread 0 posts the byte count; the transaction count may run ahead of it.
 __device__ __forceinline__ void stage_step(const DenseParams& p, long long j, double* Fdst,
                                            double* cdst, uint64_t* bar) {
-    mbar_arrive_expect_tx(bar, DN * DN * 8 + DN * 8);
-    for (int r = 0; r < DN; r++) tma_load_1d(Fdst + r * FLD, p.F + j * DN * DN + r * DN, DN * 8, bar);
-    tma_load_1d(cdst, p.c + j * DN, DN * 8, bar);
+    const int tid = threadIdx.x;
+    fence_proxy_async_smem();  // earlier generic reads of the buffer
+    if (tid == 0) {
+        mbar_arrive_expect_tx(bar, DN * FLD * 8 + DN * 8);
+        tma_load_1d(Fdst, p.F + j * DN * FLD, DN * FLD * 8, bar);
+        tma_load_1d(cdst, p.c + j * DN, DN * 8, bar);
+    }
 }
 
-struct AggSmem {
+struct AggSmem {  // ~105 KB: two chunks per SM
     double Fb[2][DN * FLD];
-    double Pb[2][DN * FLD];
+    double Pb[DN * FLD];
     double cb[2][DN];
     double y[2][DN];
     uint64_t bar[2];
@@ -557,7 +430,7 @@ __global__ void __launch_bounds__(DTHREADS) dense_agg_kernel(const DenseParams p
     }
     __syncthreads();
     uint32_t ph[2] = {0, 0};
-    if (tid == 0) {
+    if (tid <= DN) {
         fence_proxy_async_global();
         stage_step(p, s, sm.Fb[0], sm.cb[0], &sm.bar[0]);
         if (s + 1 < e) stage_step(p, s + 1, sm.Fb[1], sm.cb[1], &sm.bar[1]);
@@ -565,39 +438,87 @@ __global__ void __launch_bounds__(DTHREADS) dense_agg_kernel(const DenseParams p
     mbar_wait(&sm.bar[0], ph[0]);
     ph[0] ^= 1;
     // P = F_s, y = c_s
-    for (int q = tid; q < DN * FLD; q += DTHREADS) sm.Pb[0][q] = sm.Fb[0][q];
+    for (int q = tid; q < DN * FLD; q += DTHREADS) sm.Pb[q] = sm.Fb[0][q];
     if (tid < DN) sm.y[0][tid] = sm.cb[0][tid];
     __syncthreads();
     // buffer 0 (step s) is consumed: prefetch step s + 2 into it
-    if (tid == 0 && s + 2 < e) stage_step(p, s + 2, sm.Fb[0], sm.cb[0], &sm.bar[0]);
-    int pb = 0, yb = 0;
+    if (tid <= DN && s + 2 < e) stage_step(p, s + 2, sm.Fb[0], sm.cb[0], &sm.bar[0]);
+    int yb = 0;
     for (long long j = s + 1; j < e; j++) {
         const int fb = (int)((j - s) & 1);
         mbar_wait(&sm.bar[fb], ph[fb]);
         ph[fb] ^= 1;
-        gemm64_dmma(sm.Fb[fb], sm.Pb[pb], sm.Pb[pb ^ 1]);
+        double acc[8][2];
+        gemm64_dmma_acc(sm.Fb[fb], sm.Pb, acc);
         matvec64(sm.Fb[fb], sm.y[yb], sm.cb[fb], sm.y[yb ^ 1]);
-        __syncthreads();
+        __syncthreads();  // every read of P and F_j done
+        gemm64_store(sm.Pb, acc);
         // F_j / c_j consumed: prefetch step j + 2 into this buffer
-        if (tid == 0 && j + 2 < e) stage_step(p, j + 2, sm.Fb[fb], sm.cb[fb], &sm.bar[fb]);
-        pb ^= 1;
+        if (tid <= DN && j + 2 < e) stage_step(p, j + 2, sm.Fb[fb], sm.cb[fb], &sm.bar[fb]);
+        __syncthreads();  // P = F_j P visible
         yb ^= 1;
     }
-    for (int q = tid; q < DN * DN; q += DTHREADS) {
-        const int r = q / DN, col = q % DN;
-        p.aggP[(long long)c * DN * DN + q] = sm.Pb[pb][r * FLD + col];
-    }
+    for (int q = tid; q < DN * FLD; q += DTHREADS) p.aggP[(long long)c * DN * FLD + q] = sm.Pb[q];
     if (tid < DN) p.aggy[(long long)c * DN + tid] = sm.y[yb][tid];
+}
+
+// =========================================================================
+// K3: incoming states of the chunks  z_{c+1} = P_c z_c + y_c  (one CTA)
+// =========================================================================
+struct FoldSmem {
+    double Ab[2][DN * FLD];
+    double ab[2][DN];
+    double z[2][DN];
+    uint64_t bar[2];
+};
+
+__global__ void __launch_bounds__(DTHREADS) dense_fold_kernel(const DenseParams p) {
+    if (p.st && p.st->stopped) return;
+    extern __shared__ __align__(16) unsigned char raw[];
+    FoldSmem& sm = *reinterpret_cast<FoldSmem*>(raw);
+    const int tid = threadIdx.x;
+    const int C = p.nchunks;
+    if (tid == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < DN) {
+        sm.z[0][tid] = 0.0;  // the state before step 0
+        p.zin[tid] = 0.0;
+    }
+    __syncthreads();
+    auto stage_agg = [&](int q, int b) {
+        if (tid == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&sm.bar[b], DN * FLD * 8 + DN * 8);
+            tma_load_1d(sm.Ab[b], p.aggP + (long long)q * DN * FLD, DN * FLD * 8, &sm.bar[b]);
+            tma_load_1d(sm.ab[b], p.aggy + (long long)q * DN, DN * 8, &sm.bar[b]);
+        }
+    };
+    if (tid == 0) fence_proxy_async_global();
+    if (C > 1) stage_agg(0, 0);
+    if (C > 2) stage_agg(1, 1);
+    uint32_t ph[2] = {0, 0};
+    int zb = 0;
+    for (int q = 0; q + 1 < C; q++) {
+        const int b = q & 1;
+        mbar_wait(&sm.bar[b], ph[b]);
+        ph[b] ^= 1;
+        matvec64(sm.Ab[b], sm.z[zb], sm.ab[b], sm.z[zb ^ 1]);
+        __syncthreads();
+        if (q + 3 < C) stage_agg(q + 2, b);
+        zb ^= 1;
+        if (tid < DN) p.zin[(long long)(q + 1) * DN + tid] = sm.z[zb][tid];
+    }
 }
 
 // =========================================================================
 // K4: chunk fix-up  p_j = F_j p_{j-1} + c_j,  X_next = X + p
 // =========================================================================
-struct FixSmem {
+struct FixSmem {  // ~71 KB
     double Fb[2][DN * FLD];
-    double Ab[2][DN * FLD];  // chunk aggregates for the incoming state
     double cb[2][DN];
-    double ab[2][DN];
     double z[2][DN];
     uint64_t bar[2];
     double red[DTHREADS / 32];
@@ -617,33 +538,12 @@ __global__ void __launch_bounds__(DTHREADS) dense_fixup_kernel(const DenseParams
         mbar_init(&sm.bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < DN) sm.z[0][tid] = 0.0;  // the state before step 0
+    if (tid < DN) sm.z[0][tid] = p.zin[(long long)c * DN + tid];  // state before the chunk
     __syncthreads();
     uint32_t ph[2] = {0, 0};
-    // ---- incoming state: fold the aggregates of chunks 0..c-1 ---------------
-    auto stage_agg = [&](int q, int b) {
-        mbar_arrive_expect_tx(&sm.bar[b], DN * DN * 8 + DN * 8);
-        for (int r = 0; r < DN; r++)
-            tma_load_1d(&sm.Ab[b][r * FLD], p.aggP + (long long)q * DN * DN + r * DN, DN * 8, &sm.bar[b]);
-        tma_load_1d(sm.ab[b], p.aggy + (long long)q * DN, DN * 8, &sm.bar[b]);
-    };
-    if (tid == 0) {
-        fence_proxy_async_global();
-        if (c > 0) stage_agg(0, 0);
-        if (c > 1) stage_agg(1, 1);
-    }
     int zb = 0;
-    for (int q = 0; q < c; q++) {
-        const int b = q & 1;
-        mbar_wait(&sm.bar[b], ph[b]);
-        ph[b] ^= 1;
-        matvec64(sm.Ab[b], sm.z[zb], sm.ab[b], sm.z[zb ^ 1]);
-        __syncthreads();
-        if (tid == 0 && q + 2 < c) stage_agg(q + 2, b);
-        zb ^= 1;
-    }
     // ---- the chunk's own recursion ---------------------------------------------
-    if (tid == 0) {
+    if (tid <= DN) {
         stage_step(p, s, sm.Fb[0], sm.cb[0], &sm.bar[0]);
         if (s + 1 < e) stage_step(p, s + 1, sm.Fb[1], sm.cb[1], &sm.bar[1]);
     }
@@ -654,7 +554,7 @@ __global__ void __launch_bounds__(DTHREADS) dense_fixup_kernel(const DenseParams
         ph[fb] ^= 1;
         matvec64(sm.Fb[fb], sm.z[zb], sm.cb[fb], sm.z[zb ^ 1]);
         __syncthreads();
-        if (tid == 0 && j + 2 < e) stage_step(p, j + 2, sm.Fb[fb], sm.cb[fb], &sm.bar[fb]);
+        if (tid <= DN && j + 2 < e) stage_step(p, j + 2, sm.Fb[fb], sm.cb[fb], &sm.bar[fb]);
         zb ^= 1;
         if (tid < DN) Xn[j * DN + tid] = Xc[j * DN + tid] + sm.z[zb][tid];
         if (w == 0) step = nan_drop_max(step, warp_row_rule64(sm.z[zb][lane], sm.z[zb][lane + 32]));
@@ -704,18 +604,25 @@ static bool is_dense(const odx_problem* P, const odx_stepper* S) {
 
 int dense_supported(const odx_problem* P, const odx_stepper* S) { return is_dense(P, S) ? 1 : 0; }
 
-static size_t build_smem() { return (size_t)(DN * GJLD + 3 * DN) * sizeof(double); }
 static size_t lu_smem() { return LU_WARPS * sizeof(LuWarpSmem); }
+// chunks of the trajectory for K2/K4: two per SM (the aggregate kernel keeps
+// two chunk chains resident per SM); ODX_DENSE_CHUNKS overrides (tuning)
+static int dense_chunks() {
+    const char* e = getenv("ODX_DENSE_CHUNKS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 2 * num_sms();
+}
 
 struct DenseLayout {
-    size_t total, F, c, aggP, aggy, red, st, Xalt, flist, fcount;
+    size_t total, F, c, aggP, aggy, zin, red, st, Xalt, flist, fcount;
     DenseLayout(long long N, int C, int max_iters, bool with_X) {
         size_t off = 0;
         auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
-        F = at((size_t)N * DN * DN * 8);
+        F = at((size_t)N * DN * FLD * 8);  // rows padded to FLD: one bulk copy per step
         c = at((size_t)N * DN * 8);
-        aggP = at((size_t)C * DN * DN * 8);
+        aggP = at((size_t)C * DN * FLD * 8);
         aggy = at((size_t)C * DN * 8);
+        zin = at((size_t)C * DN * 8);
         red = at(4 * ((size_t)max_iters + 1) * 8);
         st = at(sizeof(DenseState));
         Xalt = with_X ? at((size_t)N * DN * 8) : 0;
@@ -735,7 +642,7 @@ int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, voi
                 size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
     (void)P;
     (void)S;
-    const int C = num_sms();
+    const int C = dense_chunks();
     const DenseLayout lay(sp.N, C, sp.max_iters, true);
     if (query) {
         *need = lay.total;
@@ -762,9 +669,11 @@ int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, voi
     p.status = sp.status;
     p.sidx = sp.sidx;
     p.F = reinterpret_cast<double*>(base + lay.F);
+    p.fld = FLD;
     p.c = reinterpret_cast<double*>(base + lay.c);
     p.aggP = reinterpret_cast<double*>(base + lay.aggP);
     p.aggy = reinterpret_cast<double*>(base + lay.aggy);
+    p.zin = reinterpret_cast<double*>(base + lay.zin);
     p.red = reinterpret_cast<unsigned long long*>(base + lay.red);
     p.st = reinterpret_cast<DenseState*>(base + lay.st);
     p.nchunks = (int)((sp.N < C) ? sp.N : C);
@@ -781,6 +690,8 @@ int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, voi
     if (rc) return rc;
     rc = set_smem(dense_fixup_kernel, sizeof(FixSmem));
     if (rc) return rc;
+    rc = set_smem(dense_fold_kernel, sizeof(FoldSmem));
+    if (rc) return rc;
     int per_sm = 0;
     ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BAND_WARPS * 32, 0));
     long long gb = (long long)(per_sm < 1 ? 1 : per_sm) * num_sms();
@@ -794,8 +705,9 @@ int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, voi
         launches += 3;
         if (it < sp.max_iters) {
             dense_agg_kernel<<<p.nchunks, DTHREADS, sizeof(AggSmem), st>>>(p);
+            dense_fold_kernel<<<1, DTHREADS, sizeof(FoldSmem), st>>>(p);
             dense_fixup_kernel<<<p.nchunks, DTHREADS, sizeof(FixSmem), st>>>(p, it);
-            launches += 2;
+            launches += 3;
         }
     }
     dense_final_copy_kernel<<<(unsigned)(2 * num_sms()), 256, 0, st>>>(p);
@@ -821,6 +733,7 @@ int dense_build_op(const odx_problem* P, const odx_stepper* S, const StepCoefs& 
     p.X = const_cast<double*>(X);
     p.N = N;
     p.F = Fe;
+    p.fld = DN;
     p.c = ce;
     p.h = h;
     p.first_bad = first_bad;
