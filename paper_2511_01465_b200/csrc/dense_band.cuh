@@ -55,15 +55,16 @@ __device__ __forceinline__ double bsub(double a, double m, double u) {
 // Factorise the band matrix held in W (all lanes, identical values) and solve
 // c = A^{-1}(-h) (W.c = -h on entry, the result on exit).  Returns 0 on success,
 // 1 + k for a singular pivot k, -1 when a row swap would be needed.
-__device__ __noinline__ int band_factor_solve_c(BandWarpSmem& W) {
+__device__ __forceinline__ int band_factor_solve_c(BandWarpSmem& W) {
+    const volatile BandWarpSmem& V = W;  // reads stay next to their use (see band_solve_col)
     double x[BAND_N];
     double chk = 0.0;  // becomes NaN if any factor entry is inf / NaN
 #pragma unroll
     for (int i = 0; i < BAND_N; i++) x[i] = W.c[i];
-    double d = W.Ad[0];        // running A[k][k]
-    double s = W.Al[0];        // running A[k][63]  (row 0: periodic corner)
-    double r = W.Au[63];       // running A[63][k]  (row 63: periodic corner)
-    double r63 = W.Ad[63];     // running A[63][63]
+    double d = V.Ad[0];        // running A[k][k]
+    double s = V.Al[0];        // running A[k][63]  (row 0: periodic corner)
+    double r = V.Au[63];       // running A[63][k]  (row 63: periodic corner)
+    double r63 = V.Ad[63];     // running A[63][63]
     int status = 0;            // no early exits: the loop must unroll fully
 #pragma unroll
     for (int k = 0; k < BAND_N - 1; k++) {
@@ -74,7 +75,7 @@ __device__ __noinline__ int band_factor_solve_c(BandWarpSmem& W) {
             double best = fabs(akk);
             int p = k;
             if (k < BAND_N - 2) {
-                const double v1 = fabs(W.Al[k + 1]);
+                const double v1 = fabs(V.Al[k + 1]);
                 if (v1 > best) {
                     best = v1;
                     p = k + 1;
@@ -93,9 +94,9 @@ __device__ __noinline__ int band_factor_solve_c(BandWarpSmem& W) {
                 const double inv = 1.0 / akk;
                 W.Ud[k] = akk;
                 if (k < BAND_N - 2) {
-                    const double m1 = W.Al[k + 1] * inv;
+                    const double m1 = V.Al[k + 1] * inv;
                     const double m2 = r * inv;
-                    const double uk = W.Au[k];
+                    const double uk = V.Au[k];
                     W.L1[k] = m1;
                     W.Lr[k] = m2;
                     W.Us[k] = s;
@@ -104,11 +105,11 @@ __device__ __noinline__ int band_factor_solve_c(BandWarpSmem& W) {
                     chk = fma(s, 0.0, chk);
                     chk = fma(uk, 0.0, chk);
                     // row k+1: diagonal and column 63
-                    const double dn = bsub(W.Ad[k + 1], m1, uk);
-                    const double s_init = (k + 1 == BAND_N - 2) ? W.Au[BAND_N - 2] : 0.0;
+                    const double dn = bsub(V.Ad[k + 1], m1, uk);
+                    const double s_init = (k + 1 == BAND_N - 2) ? V.Au[BAND_N - 2] : 0.0;
                     const double sn = bsub(s_init, m1, s);
                     // row 63: column k+1 and column 63
-                    const double r_init = (k + 1 == BAND_N - 2) ? W.Al[BAND_N - 1] : 0.0;
+                    const double r_init = (k + 1 == BAND_N - 2) ? V.Al[BAND_N - 1] : 0.0;
                     const double rn = bsub(r_init, m2, uk);
                     r63 = bsub(r63, m2, s);
                     // c: forward elimination with the same multipliers
@@ -137,13 +138,13 @@ __device__ __noinline__ int band_factor_solve_c(BandWarpSmem& W) {
     W.Ud[BAND_N - 1] = d;
     if (isnan(fma(d, 0.0, chk))) return -1;  // non-finite factors: exact path
     // back substitution for c
-    x[BAND_N - 1] = x[BAND_N - 1] / W.Ud[BAND_N - 1];
-    x[BAND_N - 2] = bsub(x[BAND_N - 2], W.Us[BAND_N - 2], x[BAND_N - 1]) / W.Ud[BAND_N - 2];
+    x[BAND_N - 1] = x[BAND_N - 1] / V.Ud[BAND_N - 1];
+    x[BAND_N - 2] = bsub(x[BAND_N - 2], V.Us[BAND_N - 2], x[BAND_N - 1]) / V.Ud[BAND_N - 2];
 #pragma unroll
     for (int i = BAND_N - 3; i >= 0; i--) {
-        double acc = bsub(x[i], W.Au[i], x[i + 1]);
-        acc = bsub(acc, W.Us[i], x[BAND_N - 1]);
-        x[i] = acc / W.Ud[i];
+        double acc = bsub(x[i], V.Au[i], x[i + 1]);
+        acc = bsub(acc, V.Us[i], x[BAND_N - 1]);
+        x[i] = acc / V.Ud[i];
     }
 #pragma unroll
     for (int i = 0; i < BAND_N; i++) W.c[i] = x[i];

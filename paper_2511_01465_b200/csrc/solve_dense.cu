@@ -6,19 +6,19 @@
 // c = A^{-1}(-h), then a Blelloch scan whose combines are 64x64 GEMMs
 // (~1.24 MFLOP per step).  Here, per iteration:
 //
-//   K1 dense_build    one CTA per step (grid-stride): Gauss-Jordan with partial
-//                     pivoting on [A | B | -h] (64 x 129, shared memory) gives
-//                     F = A^{-1} B and c = A^{-1}(-h) in one elimination.  The
-//                     A columns use non-contracted products, so pivot choices
-//                     and the 1e-300 singular-block test are the reference's
-//                     (GJ applies LU's exact updates to the rows below a pivot).
-//   decide            one thread: solve()'s decision (newton_pint.py:373-394)
-//   K2 dense_agg      one CTA per contiguous chunk: P <- F_j P chained with
-//                     fp64 DMMA tiles (mma.sync m8n8k4, SASS DMMA) on padded
-//                     smem operands, F_j rows TMA-staged (double-buffered)
-//   K4 dense_fixup    one CTA per chunk: incoming state from the preceding
-//                     chunk aggregates, then p_j = F_j p_{j-1} + c_j across the
-//                     chunk, X_next = X + p, max|dx| reduction
+//   K1  dense_band_build  one warp per step: the reference's LU and solves
+//                         restricted to their non-trivial operations for a
+//                         periodic-tridiagonal A with diagonal pivots
+//                         (dense_band.cuh); F rows written padded (FLD)
+//   K1b dense_lu_build    the exact sparsity-aware warp LU (dense_lu.cuh) for
+//                         the steps K1 handed off (row swaps, non-finite values)
+//   decide                one thread: solve()'s decision (newton_pint.py:373-394)
+//   K2  dense_agg         two chunk chains per SM: P <- F_j P with fp64 DMMA
+//                         (mma.sync m8n8k4, SASS DMMA) on padded smem operands,
+//                         each F_j one TMA bulk copy (double-buffered)
+//   K3  dense_fold        one CTA: chunk input states z_{c+1} = P_c z_c + y_c
+//   K4  dense_fixup       per chunk: p_j = F_j p_{j-1} + c_j from z_c,
+//                         X_next = X + p, max|dx| reduction
 //
 // The host enqueues every iteration up front; the kernels of an iteration
 // after the stop decision return immediately (no host synchronisation).
@@ -216,7 +216,7 @@ dense_lu_build_kernel(const DenseParams p, int it) {
 // K1 fast path: periodic-tridiagonal band LU, one warp per step (dense_band.cuh)
 // =========================================================================
 template <class DP>
-__global__ void __launch_bounds__(BAND_WARPS * 32)
+__global__ void __launch_bounds__(BAND_WARPS * 32, 3)
 dense_band_build_kernel(const DenseParams p, int it) {
     if (p.st && p.st->stopped) return;
     __shared__ BandWarpSmem bsm[BAND_WARPS];
