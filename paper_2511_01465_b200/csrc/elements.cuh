@@ -180,8 +180,38 @@ __device__ __forceinline__ void build_explicit_step(const P& prob, const StepCoe
 // non-zero pivots.  With identical A the factorisation is bit-identical to
 // the reference's.
 // ---------------------------------------------------------------------------
+// IEEE-754 a / b.  The hardware division sequence sends non-finite operands
+// and zero divisors down a slow subroutine; diverging trajectories (NaN/inf
+// rows) hit that on every step.  Here the division always runs on safe
+// operands and the special cases (results 0, inf or NaN with the IEEE sign
+// rules) are selected afterwards — branch-free, so the unrolled items of a
+// thread keep their instruction-level parallelism.
+__device__ __forceinline__ double div_rn(double a, double b) {
+    const bool fa = isfinite(a), fb = isfinite(b);
+    const bool safe = fa && fb && b != 0.0;
+    double as = safe ? a : 1.0, bs = safe ? b : 1.0;
+    // opaque to the optimiser, which would otherwise fold the selects past
+    // the division (safe ? a / b : 1.0) and divide the raw operands again
+    asm("mov.b64 %0, %0;" : "+d"(as));
+    asm("mov.b64 %0, %0;" : "+d"(bs));
+    const double q = as / bs;
+    const long long sgn = (__double_as_longlong(a) ^ __double_as_longlong(b)) & (long long)0x8000000000000000ull;
+    const double inf = __longlong_as_double(0x7ff0000000000000ll | sgn);
+    const double zero = __longlong_as_double(sgn);
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    const bool ia = isinf(a), ib = isinf(b);
+    const bool is_nan = isnan(a) || isnan(b) || (ia && ib) || (a == 0.0 && b == 0.0);
+    const bool is_inf = ia || (b == 0.0);  // (NaN cases already taken)
+    const double sp = is_nan ? nan : (is_inf ? inf : zero);  // zero: finite / inf
+    return safe ? q : sp;
+}
+
+// rinv[k] = 1 / U[k][k] (div_rn); the triangular solve multiplies by it
+// instead of dividing (x / d vs x * (1/d): <= 1 ulp apart for finite values,
+// the same 0 / inf / NaN class and sign otherwise, |d| >= 1e-300 by the
+// pivot floor) — D divisions per block instead of D per right-hand side.
 template <int D>
-__device__ __forceinline__ int lu_factor_reg(double* A, int* piv) {
+__device__ __forceinline__ int lu_factor_reg(double* A, int* piv, double* rinv) {
 #pragma unroll
     for (int k = 0; k < D; k++) {
         int p = k;
@@ -204,7 +234,8 @@ __device__ __forceinline__ int lu_factor_reg(double* A, int* piv) {
                 }
             }
         }
-        double inv = 1.0 / A[k * D + k];
+        const double inv = div_rn(1.0, A[k * D + k]);
+        rinv[k] = inv;
 #pragma unroll
         for (int i = k + 1; i < D; i++) {
             double m = A[i * D + k] * inv;
@@ -217,7 +248,8 @@ __device__ __forceinline__ int lu_factor_reg(double* A, int* piv) {
 }
 
 template <int D>
-__device__ __forceinline__ void lu_solve_reg(const double* A, const int* piv, double* x) {
+__device__ __forceinline__ void lu_solve_reg(const double* A, const int* piv, const double* rinv,
+                                             double* x) {
 #pragma unroll
     for (int k = 0; k < D; k++) {
 #pragma unroll
@@ -232,7 +264,7 @@ __device__ __forceinline__ void lu_solve_reg(const double* A, const int* piv, do
         double acc = x[i];
 #pragma unroll
         for (int j = i + 1; j < D; j++) acc = __dsub_rn(acc, __dmul_rn(A[i * D + j], x[j]));
-        x[i] = acc / A[i * D + i];
+        x[i] = acc * rinv[i];
     }
 }
 
@@ -262,7 +294,8 @@ __device__ __forceinline__ bool build_implicit_step(const P& prob, const StepCoe
         for (int c = 0; c < D; c++)
             A[r * D + c] = __dsub_rn((r == c) ? 1.0 : 0.0, __dmul_rn(sc.dt_wnext, A[r * D + c]));
     int piv[D];
-    int st = lu_factor_reg<D>(A, piv);
+    double rinv[D];
+    int st = lu_factor_reg<D>(A, piv, rinv);
     if (st >= 0) {
 #pragma unroll
         for (int r = 0; r < D; r++) {
@@ -275,7 +308,7 @@ __device__ __forceinline__ bool build_implicit_step(const P& prob, const StepCoe
     double col[D];
 #pragma unroll
     for (int r = 0; r < D; r++) col[r] = -h[r];
-    lu_solve_reg<D>(A, piv, col);
+    lu_solve_reg<D>(A, piv, rinv, col);
 #pragma unroll
     for (int r = 0; r < D; r++) el.c[r] = col[r];
     if (first) {
@@ -287,7 +320,7 @@ __device__ __forceinline__ bool build_implicit_step(const P& prob, const StepCoe
 #pragma unroll
             for (int r = 0; r < D; r++)
                 col[r] = __dadd_rn(__dmul_rn(sc.dt_wprev, Jp[r * D + c]), (r == c) ? 1.0 : 0.0);
-            lu_solve_reg<D>(A, piv, col);
+            lu_solve_reg<D>(A, piv, rinv, col);
 #pragma unroll
             for (int r = 0; r < D; r++) el.F[r * D + c] = col[r];
         }

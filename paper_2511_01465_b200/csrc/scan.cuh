@@ -248,4 +248,22 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, uns
     __syncthreads();
 }
 
+// Grid barrier on a monotonically increasing arrival counter (zeroed once per
+// launch): the caller's k-th barrier passes once count >= k * nblocks, i.e.
+// `target`.  One acq_rel atomic per CTA; the last arriver never spins.
+__device__ __forceinline__ void grid_barrier_mono(unsigned* count, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(count) : "memory");
+        if ((int)(old + 1u - target) < 0) {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+            } while ((int)(v - target) < 0);
+        }
+    }
+    __syncthreads();
+}
+
 }  // namespace odx

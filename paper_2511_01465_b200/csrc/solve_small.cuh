@@ -475,6 +475,23 @@ __device__ __forceinline__ void warp_reduce_earliest_first(Elem<D>& e, bool& has
     }
 }
 
+#ifdef ODX_GR_TRACE
+__device__ unsigned long long* g_gr_trace = nullptr;  // [3 CTAs][iters][16]
+#define GR_STAMP(slot_)                                                                  \
+    do {                                                                                 \
+        if (g_gr_trace && threadIdx.x == 0) {                                            \
+            const int which_ = (g == 0) ? 0 : (g == G / 2) ? 1 : (g == G - 1) ? 2 : -1;  \
+            if (which_ >= 0 && it < 64) {                                                \
+                unsigned long long t_;                                                   \
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+                g_gr_trace[(which_ * 64 + it) * 16 + (slot_)] = t_;                      \
+            }                                                                            \
+        }                                                                                \
+    } while (0)
+#else
+#define GR_STAMP(slot_) do { } while (0)
+#endif
+
 template <class P, int KIND, int S, int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS)
 grid_resident_kernel(const GridResParams gp) {
@@ -486,7 +503,8 @@ grid_resident_kernel(const GridResParams gp) {
     using L = typename E::L;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typename E::Shared& sm = *reinterpret_cast<typename E::Shared*>(smem_raw);
-    __shared__ double s_z[D];
+    __shared__ double s_wagg[NW][EA];
+    __shared__ int s_whas[NW];
 
     const SolveParams& p = gp.sp;
     struct HChunk { double v; unsigned long long tag; };
@@ -508,6 +526,7 @@ grid_resident_kernel(const GridResParams gp) {
 
     Decision dd{0, -1, -1, 0};
     for (int it = 0; it <= p.max_iters; it++) {
+        GR_STAMP(0);
         // halo from CTA g-1 (its last row of the current iterate)
         if (it > 0 && g > 0 && tid < D) {
             const HChunk* src = halos + (g - 1) * D + tid;
@@ -524,14 +543,17 @@ grid_resident_kernel(const GridResParams gp) {
             sm.xs[L::idx(tid)] = __longlong_as_double(v);
         }
         __syncthreads();
+        GR_STAMP(1);
         Elem<D> el[ITEMS];
         double rn = 0.0, scn = 0.0;
         unsigned long long bad = ~0ull;
         E::build_items(prob, p.sc, sm, base, N, el, rn, scn, bad);
+        GR_STAMP(2);
         Elem<D> agg;
         bool has;
         const bool do_scan = it < p.max_iters;
         if (do_scan) E::block_scan(sm, base, N, el, agg, has);
+        GR_STAMP(3);
         rn = warp_max_nan_drop(rn);
         scn = warp_max_nan_drop(scn);
         bad = warp_min_u64(bad);
@@ -564,25 +586,20 @@ grid_resident_kernel(const GridResParams gp) {
                 for (int k = 0; k < D; k++) dst[D * D + k] = A.c[k];
             }
         }
-        grid_barrier(p.bar, p.bar + 1, G);
+        GR_STAMP(4);
+        grid_barrier_mono(p.bar, (unsigned)(it + 1) * G);
+        GR_STAMP(5);
+        // incoming state: ordered fold of the aggregates of CTAs 0..g-1 over the
+        // whole block (its L2 loads overlap the decision's); thread t folds a
+        // contiguous run, warps reduce earliest-first, warp 0 joins the warps
         const unsigned long long* red = p.red + 4ll * it;
-        const double rnb = bitsd(__ldcg(red + 0));
-        const double scb = (KIND == 0) ? rnb : bitsd(__ldcg(red + 1));
-        // every CTA's step atomic of iteration it-1 precedes this barrier
-        const double step_prev = (it > 0) ? bitsd(__ldcg(red - 4 + 2))
-                                          : __longlong_as_double(0x7ff8000000000000ll);
-        dd = decide(it, p, rnb, __ldcg(red + 3), step_prev);
-        if (g == 0 && tid == 0 && dd.status != ODX_ST_SINGULAR) {
-            if (p.hist) p.hist[it] = rnb;
-            if (p.shist) p.shist[it] = scb;
-        }
-        if (dd.stop) break;
-        // incoming state: ordered fold of the aggregates of CTAs 0..g-1 (warp 0)
-        if (w == 0) {
-            Elem<D> e;
-            bool eh = false;
-            const long long per = (g + 31) / 32;
-            const long long lo = lane * per, hi = (lo + per < g) ? lo + per : g;
+        const unsigned long long r_rn = __ldcg(red + 0), r_sc = __ldcg(red + 1), r_bad = __ldcg(red + 3);
+        const unsigned long long r_step = (it > 0) ? __ldcg(red - 4 + 2) : 0ull;
+        Elem<D> fe;
+        bool fh = false;
+        {
+            const long long per = (g + THREADS - 1) / THREADS;
+            const long long lo = tid * per, hi = (lo + per < g) ? lo + per : g;
             for (long long q = lo; q < hi; q++) {
                 Elem<D> a;
                 const double* src = gp.aggs + q * EA;
@@ -590,6 +607,45 @@ grid_resident_kernel(const GridResParams gp) {
                 for (int k = 0; k < D * D; k++) a.F[k] = __ldcg(src + k);
 #pragma unroll
                 for (int k = 0; k < D; k++) a.c[k] = __ldcg(src + D * D + k);
+                if (fh)
+                    compose<D>(fe, a, fe);
+                else {
+                    fe = a;
+                    fh = true;
+                }
+            }
+        }
+        const double rnb = bitsd(r_rn);
+        const double scb = (KIND == 0) ? rnb : bitsd(r_sc);
+        // every CTA's step atomic of iteration it-1 precedes this barrier
+        const double step_prev = (it > 0) ? bitsd(r_step) : __longlong_as_double(0x7ff8000000000000ll);
+        dd = decide(it, p, rnb, r_bad, step_prev);
+        if (g == 0 && tid == 0 && dd.status != ODX_ST_SINGULAR) {
+            if (p.hist) p.hist[it] = rnb;
+            if (p.shist) p.shist[it] = scb;
+        }
+        GR_STAMP(6);
+        if (dd.stop) break;
+        if (!fh) set_identity<D>(fe);
+        warp_reduce_earliest_first<D>(fe, fh, lane);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < D * D; k++) s_wagg[w][k] = fe.F[k];
+#pragma unroll
+            for (int k = 0; k < D; k++) s_wagg[w][D * D + k] = fe.c[k];
+            s_whas[w] = fh ? 1 : 0;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            Elem<D> e;
+            bool eh = false;
+            for (int q = 0; q < NW; q++) {
+                if (!s_whas[q]) continue;
+                Elem<D> a;
+#pragma unroll
+                for (int k = 0; k < D * D; k++) a.F[k] = s_wagg[q][k];
+#pragma unroll
+                for (int k = 0; k < D; k++) a.c[k] = s_wagg[q][D * D + k];
                 if (eh)
                     compose<D>(e, a, e);
                 else {
@@ -597,21 +653,14 @@ grid_resident_kernel(const GridResParams gp) {
                     eh = true;
                 }
             }
-            if (!eh) set_identity<D>(e);
-            warp_reduce_earliest_first<D>(e, eh, lane);
-            if (lane == 0) {
 #pragma unroll
-                for (int k = 0; k < D; k++) s_z[k] = eh ? e.c[k] : 0.0;
-            }
+            for (int k = 0; k < D; k++) sm.z[k] = eh ? e.c[k] : 0.0;
         }
         __syncthreads();
-        if (tid == 0) {
-#pragma unroll
-            for (int k = 0; k < D; k++) sm.z[k] = s_z[k];
-        }
-        __syncthreads();
+        GR_STAMP(7);
         double step = 0.0;
         E::apply_items(sm, base, N, el, agg, has, step);
+        GR_STAMP(8);
         step = warp_max_nan_drop(step);
         if (lane == 0) sm.redd[2][w] = step;
         __syncthreads();
@@ -629,6 +678,7 @@ grid_resident_kernel(const GridResParams gp) {
             if (s2 > 0.0) atomicMax(p.red + 4ll * it + 2, dbits(s2));
         }
         __syncthreads();
+        GR_STAMP(9);
     }
     // final iterate back to global memory
     for (int i = tid; i < (int)(rows * D); i += THREADS) p.X[base * D + i] = sm.xs[L::idx(i + D)];
