@@ -138,6 +138,27 @@ struct SmallEngine {
         }
     }
 
+    // One item (step base + tid*ITEMS + i) of build_items.
+    __device__ __forceinline__ static void build_item(const P& prob, const StepCoefs& sc,
+                                                      const Shared& sm, long long base, long long N,
+                                                      int i, Elem<D>& el, double& rn, double& scn,
+                                                      unsigned long long& bad) {
+        const int r = threadIdx.x * ITEMS + i;
+        const long long k = base + r;
+        if (k < N) {
+            double prev[D], xk[D], h[D];
+#pragma unroll
+            for (int j = 0; j < D; j++) {
+                prev[j] = sm.xs[L::idx(r * D + j)];
+                xk[j] = sm.xs[L::idx((r + 1) * D + j)];
+            }
+            bool sing = build_step<P, KIND, S>(prob, sc, prev, xk, k == 0, el, h);
+            rn = nan_drop_max(rn, row_max_abs<D>(h));
+            if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(el.c));
+            if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
+        }
+    }
+
     // Fold this thread's items, scan the block, and leave the warp totals in
     // shared memory.  Returns the thread inclusive aggregate (within its warp).
     __device__ __forceinline__ static void block_scan(Shared& sm, long long base, long long N,
@@ -525,29 +546,39 @@ grid_resident_kernel(const GridResParams gp) {
     __syncthreads();
 
     Decision dd{0, -1, -1, 0};
+    bool step_pending = false;
     for (int it = 0; it <= p.max_iters; it++) {
         GR_STAMP(0);
-        // halo from CTA g-1 (its last row of the current iterate)
-        if (it > 0 && g > 0 && tid < D) {
-            const HChunk* src = halos + (g - 1) * D + tid;
-            const unsigned long long want = (unsigned long long)it;
-            unsigned long long tag;
-            long long v;
-            int spins = 0;
-            while (true) {
-                asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
-                             : "=l"(v), "=l"(tag) : "l"(src) : "memory");
-                if (tag == want) break;
-                if (++spins > 8) __nanosleep(20);
-            }
-            sm.xs[L::idx(tid)] = __longlong_as_double(v);
-        }
-        __syncthreads();
+        __syncthreads();  // the last apply's rows are visible to every thread
         GR_STAMP(1);
         Elem<D> el[ITEMS];
         double rn = 0.0, scn = 0.0;
         unsigned long long bad = ~0ull;
-        E::build_items(prob, p.sc, sm, base, N, el, rn, scn, bad);
+        // items in the order 1..ITEMS-1, 0: thread 0's item 0 needs the halo
+        // from CTA g-1 (its last row of the current iterate), whose arrival
+        // then overlaps the thread's other items
+#pragma unroll
+        for (int ii = 0; ii < ITEMS; ii++) {
+            const int i = (ii + 1) % ITEMS;
+            if (i == 0 && tid == 0 && it > 0 && g > 0) {
+#pragma unroll
+                for (int k = 0; k < D; k++) {
+                    const HChunk* src = halos + (g - 1) * D + k;
+                    const unsigned long long want = (unsigned long long)it;
+                    unsigned long long tag;
+                    long long v;
+                    int spins = 0;
+                    while (true) {
+                        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                                     : "=l"(v), "=l"(tag) : "l"(src) : "memory");
+                        if (tag == want) break;
+                        if (++spins > 8) __nanosleep(20);
+                    }
+                    sm.xs[L::idx(k)] = __longlong_as_double(v);
+                }
+            }
+            E::build_item(prob, p.sc, sm, base, N, i, el[i], rn, scn, bad);
+        }
         GR_STAMP(2);
         Elem<D> agg;
         bool has;
@@ -575,6 +606,11 @@ grid_resident_kernel(const GridResParams gp) {
             if (a > 0.0) atomicMax(red + 0, dbits(a));
             if (c > 0.0) atomicMax(red + 1, dbits(c));
             if (m != ~0ull) atomicMin(red + 3, m);
+            if (step_pending) {  // max|dx| of iteration it-1
+                double s2 = 0.0;
+                for (int q = 0; q < NW; q++) s2 = fmax(s2, sm.redd[2][q]);
+                if (s2 > 0.0) atomicMax(red - 4 + 2, dbits(s2));
+            }
             if (do_scan) {
                 Elem<D> A;
                 bool A_has = false;
@@ -661,23 +697,23 @@ grid_resident_kernel(const GridResParams gp) {
         double step = 0.0;
         E::apply_items(sm, base, N, el, agg, has, step);
         GR_STAMP(8);
+        // the thread that owns the last row hands it to CTA g+1 (tag = next
+        // iteration) as soon as it has written it
+        if (g + 1 < G && tid == (int)((rows - 1) / ITEMS)) {
+#pragma unroll
+            for (int k = 0; k < D; k++) {
+                const double v = sm.xs[L::idx((int)rows * D + k)];
+                HChunk* dst = halos + g * D + k;
+                asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(dst),
+                             "l"(__double_as_longlong(v)), "l"((unsigned long long)(it + 1))
+                             : "memory");
+            }
+        }
+        // max|dx|: warp maxima now; the block max and its atomic ride on the
+        // next iteration's reduction (before that iteration's barrier)
         step = warp_max_nan_drop(step);
         if (lane == 0) sm.redd[2][w] = step;
-        __syncthreads();
-        // hand the new last row to CTA g+1 (tag = next iteration)
-        if (g + 1 < G && tid < D) {
-            const double v = sm.xs[L::idx((int)rows * D + tid)];
-            HChunk* dst = halos + g * D + tid;
-            asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(dst),
-                         "l"(__double_as_longlong(v)), "l"((unsigned long long)(it + 1))
-                         : "memory");
-        }
-        if (tid == 0) {
-            double s2 = 0.0;
-            for (int q = 0; q < NW; q++) s2 = fmax(s2, sm.redd[2][q]);
-            if (s2 > 0.0) atomicMax(p.red + 4ll * it + 2, dbits(s2));
-        }
-        __syncthreads();
+        step_pending = true;
         GR_STAMP(9);
     }
     // final iterate back to global memory

@@ -231,11 +231,10 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
     if (!resident && p.B == 1 && use_grid_resident()) {
         constexpr int GI = (D <= 2) ? 4 : 2;
         int rc = ODX_EUNSUPPORTED;
-        static const int gr2_per_sm = [] {
-            const char* v = std::getenv("ODX_GR2_PER_SM");
-            return v ? std::atoi(v) : 1;
-        }();
-        if (p.N <= 128LL * 2 * 148 * gr2_per_sm)
+        // one 2-item tile per SM when that covers N; else 4-item tiles
+        // (measured: more, smaller CTAs lose more to the per-iteration sync
+        // than they gain in build time)
+        if (p.N <= 128LL * 2 * 148)
             rc = launch_grid_resident<P, KIND, S, 128, 2>(p, ws, ws_bytes, st, query, need);
         if (rc == ODX_EUNSUPPORTED)
             rc = launch_grid_resident<P, KIND, S, 128, GI>(p, ws, ws_bytes, st, query, need);
