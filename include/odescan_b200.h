@@ -129,6 +129,18 @@ int odx_solve(const odx_problem* P, const odx_stepper* S,
               int32_t* iters, int32_t* status, int64_t* status_index,
               void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same solve with HOST buffers (numpy-in / numpy-out, as the reference's
+ * solve() is called): x0 (B*d), X_guess (B*N*d) in; X_out (may alias
+ * X_guess), hist / scaled_hist (B*(max_iters+1), entries past the iterations
+ * run set to NaN; may be NULL), iters, status, status_index (B) out.  One H2D
+ * and one D2H through cached pinned staging; blocks until the result is on the
+ * host.  Device buffers and workspace are cached per device (grow-only). */
+int odx_solve_host(const odx_problem* P, const odx_stepper* S,
+                   const double* x0, const double* X_guess, double* X_out,
+                   int64_t B, int64_t N, double dt, const odx_newton_cfg* C,
+                   double* hist, double* scaled_hist,
+                   int32_t* iters, int32_t* status, int64_t* status_index, void* stream);
+
 /* ---- piecewise ops mirroring the reference's compiled loops ---------------- */
 /* _kernels.build_explicit  _kernels.py:299-342 (+ _rk_increment_with_jac :261-296) */
 int odx_build_explicit(const odx_problem* P, const odx_stepper* S,

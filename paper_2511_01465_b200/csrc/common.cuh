@@ -32,6 +32,11 @@ inline int fail(int code, const char* msg) {
 int num_sms();
 void count_launch(int n = 1);
 
+// Sets the kernel's dynamic shared-memory limit and returns its resident CTAs
+// per SM, once per (kernel, block size, smem, device): both CUDA queries cost
+// microseconds that would otherwise sit on every solve's launch path.
+int kernel_occupancy(const void* kern, int threads, size_t smem, int* per_sm);
+
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // Carves a workspace into aligned sub-buffers (dry run when base is null).
@@ -50,5 +55,8 @@ struct Carver {
 bool fill_params(const odx_problem* P, ProbParams& pp);
 bool fill_coefs(const odx_stepper* S, double dt, StepCoefs& sc);
 void init_bad_slots(unsigned long long* red, int n, cudaStream_t st);
+// zero [base, base+bytes) with the first n reduction quads' bad slots = ~0
+// (base must be 8-byte aligned and start with those quads)
+void init_ws(void* base, size_t bytes, int n, cudaStream_t st);
 
 }  // namespace odx

@@ -1,0 +1,283 @@
+// host_solve.cu — odx_solve_host: the solver with HOST buffers on both sides
+// (what the reference's numpy-in / numpy-out solve() hands over), one H2D and
+// one D2H per call.  Replaces newton_pint.solve :326-406 for callers that hold
+// their guess in host memory.
+//
+// Per device a grow-only cache keeps: the device region
+//   x0 (B*d) | X (B*N*d) | outcome (hist | shist | sidx | iters | status)
+// the solver workspace, and two pinned staging blocks (in: x0 | X, out: X |
+// outcome).  A call packs the inputs into pinned memory, issues one H2D, the
+// solve, one D2H, synchronises the stream and unpacks into the caller's
+// buffers; caller buffers that are already page-locked skip the staging copy
+// (DMA to / from them directly).  Calls are serialised by a mutex (the caches
+// are shared).
+#include <atomic>
+#include <emmintrin.h>
+#include <chrono>
+#include <condition_variable>
+#include <thread>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+extern "C" {
+size_t odx_solve_workspace_bytes(const odx_problem* P, const odx_stepper* S, int64_t B, int64_t N,
+                                 const odx_newton_cfg* C);
+int odx_solve(const odx_problem* P, const odx_stepper* S, const double* x0, double* X, int64_t B,
+              int64_t N, double dt, const odx_newton_cfg* C, double* hist, double* scaled_hist,
+              int32_t* iters, int32_t* status, int64_t* status_index, void* workspace,
+              size_t workspace_bytes, void* stream);
+}
+
+namespace odx {
+namespace {
+
+struct HostCache {
+    void* dregion = nullptr;
+    size_t dbytes = 0;
+    void* ws = nullptr;
+    size_t wsbytes = 0;
+    void* pin_in = nullptr;
+    size_t in_bytes = 0;
+    void* pin_out = nullptr;
+    size_t out_bytes = 0;
+};
+
+std::mutex g_host_mu;
+std::vector<HostCache> g_host_cache;
+
+int grow_device(void** p, size_t* have, size_t need) {
+    if (*have >= need) return ODX_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    ODX_CUDA(cudaMalloc(p, need));
+    *have = need;
+    return ODX_OK;
+}
+
+int grow_pinned(void** p, size_t* have, size_t need) {
+    if (*have >= need) return ODX_OK;
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *have = 0;
+    ODX_CUDA(cudaMallocHost(p, need));
+    *have = need;
+    return ODX_OK;
+}
+
+inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// Host memcpy of the staging path split over a small persistent worker pool
+// (one core copies ~20 GB/s; the trajectory is MBs).  Workers sleep on a
+// condition variable between calls; ODX_HOST_THREADS sets the pool size
+// (default 4, 0 or 1 = plain memcpy).
+// Copy with non-temporal stores: the destination (pinned staging the DMA
+// engine reads next, or the caller's result) does not linger dirty in this
+// core's caches, so the device's reads of it need no cross-core snoops.
+inline void nt_copy(char* dst, const char* src, size_t n) {
+    size_t i = 0;
+    if (((reinterpret_cast<size_t>(dst) | reinterpret_cast<size_t>(src)) & 15) == 0) {
+        for (; i + 64 <= n; i += 64) {
+            const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+            const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+            const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+            const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+            _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+        }
+        _mm_sfence();
+    }
+    if (i < n) std::memcpy(dst + i, src + i, n - i);
+}
+
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    void copy(void* dst, const void* src, size_t n) {
+        const int T = (int)workers_.size();
+        if (T == 0 || n < (size_t(1) << 19)) {
+            nt_copy(static_cast<char*>(dst), static_cast<const char*>(src), n);
+            return;
+        }
+        const int parts = T + 1;
+        const size_t chunk = ((n + parts - 1) / parts + 63) & ~size_t(63);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            n_ = n;
+            chunk_ = chunk;
+            pending_.store(T, std::memory_order_relaxed);
+            gen_++;
+        }
+        cv_.notify_all();
+        const size_t lo = (size_t)T * chunk;  // the caller copies the last part
+        if (lo < n) nt_copy(dst_ + lo, src_ + lo, n - lo);
+        while (pending_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+    }
+
+  private:
+    CopyPool() {
+        const char* e = std::getenv("ODX_HOST_THREADS");
+        int t = e ? std::atoi(e) : 4;
+        if (t > 1)
+            for (int i = 0; i < t - 1; i++) workers_.emplace_back([this, i] { run(i); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            gen_++;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    void run(int i) {
+        unsigned long long seen = 0;
+        while (true) {
+            char* d;
+            const char* s;
+            size_t n, chunk;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                d = dst_, s = src_, n = n_, chunk = chunk_;
+            }
+            const size_t lo = (size_t)i * chunk;
+            if (lo < n) nt_copy(d + lo, s + lo, (lo + chunk < n ? chunk : n - lo));
+            pending_.fetch_sub(1, std::memory_order_release);
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t n_ = 0, chunk_ = 0;
+    std::atomic<int> pending_{0};
+};
+
+// page-locked (cudaHostAlloc / registered) host memory can be a DMA endpoint
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+}  // namespace odx
+
+extern "C" int odx_solve_host(const odx_problem* P, const odx_stepper* S, const double* x0,
+                              const double* X_guess, double* X_out, int64_t B, int64_t N,
+                              double dt, const odx_newton_cfg* C, double* hist,
+                              double* scaled_hist, int32_t* iters, int32_t* status,
+                              int64_t* status_index, void* stream) {
+    using namespace odx;
+    if (!P || !S || !C || !x0 || !X_guess || !X_out || !iters || !status || !status_index)
+        return fail(ODX_EINVAL, "null host buffer");
+    if (B < 1 || N < 1) return fail(ODX_EINVAL, "B and N must be >= 1");
+    if (C->max_iters < 0) return fail(ODX_EINVAL, "max_iters must be >= 0");
+    const int64_t d = P->dim;
+    if (d < 1) return fail(ODX_EINVAL, "bad state dimension");
+    // (invalid descriptors make the query return 0; odx_solve then reports them)
+    size_t wsb = odx_solve_workspace_bytes(P, S, B, N, C);
+    if (wsb < 256) wsb = 256;
+    const int64_t H = (int64_t)C->max_iters + 1;
+    const size_t nx0 = (size_t)(B * d) * 8, nX = (size_t)(B * N * d) * 8;
+    const size_t o_X = al256(nx0), o_out = o_X + al256(nX);
+    const size_t o_sh = (size_t)(B * H) * 8, o_sidx = 2 * o_sh, o_it = o_sidx + (size_t)B * 8,
+                 o_st = o_it + (size_t)B * 4, out_bytes = o_st + (size_t)B * 4;
+    int dev = 0;
+    ODX_CUDA(cudaGetDevice(&dev));
+    cudaStream_t st = (cudaStream_t)stream;
+
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    if ((int)g_host_cache.size() <= dev) g_host_cache.resize(dev + 1);
+    HostCache& hc = g_host_cache[dev];
+    int rc;
+    if ((rc = grow_device(&hc.dregion, &hc.dbytes, o_out + out_bytes))) return rc;
+    if ((rc = grow_device(&hc.ws, &hc.wsbytes, wsb))) return rc;
+    if ((rc = grow_pinned(&hc.pin_in, &hc.in_bytes, o_X + nX))) return rc;
+    if ((rc = grow_pinned(&hc.pin_out, &hc.out_bytes, (o_out - o_X) + out_bytes))) return rc;
+
+    static const bool timing = std::getenv("ODX_HOST_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
+    char* din = static_cast<char*>(hc.dregion);
+    char* pin = static_cast<char*>(hc.pin_in);
+    char* pout = static_cast<char*>(hc.pin_out);
+    // pinned caller buffers are DMA'd directly; pageable ones go through
+    // the cached staging blocks
+    const bool in_pinned = is_pinned(X_guess), out_pinned = is_pinned(X_out);
+    std::memcpy(pin, x0, nx0);
+    if (!in_pinned) CopyPool::get().copy(pin + o_X, X_guess, nX);
+    auto t1 = now();
+    if (in_pinned) {
+        ODX_CUDA(cudaMemcpyAsync(din, pin, nx0, cudaMemcpyHostToDevice, st));
+        ODX_CUDA(cudaMemcpyAsync(din + o_X, X_guess, nX, cudaMemcpyHostToDevice, st));
+    } else {
+        ODX_CUDA(cudaMemcpyAsync(din, pin, o_X + nX, cudaMemcpyHostToDevice, st));
+    }
+    auto t2 = now();
+    char* dout = din + o_out;
+    rc = odx_solve(P, S, reinterpret_cast<const double*>(din), reinterpret_cast<double*>(din + o_X),
+                   B, N, dt, C, reinterpret_cast<double*>(dout),
+                   reinterpret_cast<double*>(dout + o_sh), reinterpret_cast<int32_t*>(dout + o_it),
+                   reinterpret_cast<int32_t*>(dout + o_st), reinterpret_cast<int64_t*>(dout + o_sidx),
+                   hc.ws, hc.wsbytes, stream);
+    if (rc) return rc;
+    auto t3 = now();
+    if (out_pinned) {
+        ODX_CUDA(cudaMemcpyAsync(X_out, din + o_X, nX, cudaMemcpyDeviceToHost, st));
+        ODX_CUDA(cudaMemcpyAsync(pout + (o_out - o_X), din + o_out, out_bytes,
+                                 cudaMemcpyDeviceToHost, st));
+    } else {
+        ODX_CUDA(cudaMemcpyAsync(pout, din + o_X, (o_out - o_X) + out_bytes,
+                                 cudaMemcpyDeviceToHost, st));
+    }
+    auto t4 = now();
+    ODX_CUDA(cudaStreamSynchronize(st));
+    auto t5 = now();
+
+    if (!out_pinned) CopyPool::get().copy(X_out, pout, nX);
+    const char* ob = pout + (o_out - o_X);
+    std::memcpy(status_index, ob + o_sidx, (size_t)B * 8);
+    std::memcpy(iters, ob + o_it, (size_t)B * 4);
+    std::memcpy(status, ob + o_st, (size_t)B * 4);
+    // history entries past the iterations run are not written by the device
+    // loop: report them as NaN (a singular block stops before recording)
+    const double qnan = std::nan("");
+    for (int64_t b = 0; b < B; b++) {
+        const int64_t last = (status[b] == ODX_ST_SINGULAR) ? (int64_t)iters[b] - 1 : iters[b];
+        const double* hs = reinterpret_cast<const double*>(ob) + b * H;
+        const double* ss = reinterpret_cast<const double*>(ob + o_sh) + b * H;
+        for (int64_t i = 0; i < H; i++) {
+            if (hist) hist[b * H + i] = (i <= last) ? hs[i] : qnan;
+            if (scaled_hist) scaled_hist[b * H + i] = (i <= last) ? ss[i] : qnan;
+        }
+    }
+    if (timing) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "odx_solve_host us: pack %.1f h2d-enq %.1f solve-enq %.1f d2h-enq %.1f sync %.1f unpack %.1f\n",
+                     us(t0, t1), us(t1, t2), us(t2, t3), us(t3, t4), us(t4, t5), us(t5, now()));
+    }
+    return ODX_OK;
+}

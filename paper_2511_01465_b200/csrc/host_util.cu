@@ -76,3 +76,39 @@ bool fill_coefs(const odx_stepper* S, double dt, StepCoefs& sc) {
 }
 
 }  // namespace odx
+
+namespace odx {
+int kernel_occupancy(const void* kern, int threads, size_t smem, int* per_sm) {
+    struct Key {
+        const void* k;
+        int t, dev;
+        size_t s;
+        bool operator==(const Key& o) const { return k == o.k && t == o.t && dev == o.dev && s == o.s; }
+    };
+    struct Hash {
+        size_t operator()(const Key& q) const {
+            return std::hash<const void*>()(q.k) ^ (size_t(q.t) << 20) ^ (q.s << 1) ^ size_t(q.dev);
+        }
+    };
+    static std::mutex mu;
+    static std::unordered_map<Key, int, Hash> cache;
+    int dev = 0;
+    ODX_CUDA(cudaGetDevice(&dev));
+    const Key key{kern, threads, dev, smem};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *per_sm = it->second;
+            return ODX_OK;
+        }
+    }
+    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int v = 0;
+    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, threads, smem));
+    std::lock_guard<std::mutex> lock(mu);
+    cache[key] = v;
+    *per_sm = v;
+    return ODX_OK;
+}
+}  // namespace odx

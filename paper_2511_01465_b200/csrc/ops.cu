@@ -16,6 +16,24 @@ __global__ void init_bad_slots_kernel(unsigned long long* red, int n) {
     if (i < n) red[4 * i + 3] = ~0ull;
 }
 
+// Zero `words` 8-byte words at base, except the "bad" slot (4th) of each of
+// the first n reduction quads, which starts at all-ones: one launch instead of
+// a memset plus init_bad_slots.
+__global__ void init_ws_kernel(unsigned long long* base, long long words, int n) {
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < words;
+         w += (long long)gridDim.x * blockDim.x)
+        base[w] = (w < 4LL * n && (w & 3) == 3) ? ~0ull : 0ull;
+}
+
+void init_ws(void* base, size_t bytes, int n, cudaStream_t st) {
+    const long long words = (long long)((bytes + 7) / 8);
+    long long blocks = (words + 255) / 256;
+    if (blocks > 4LL * num_sms()) blocks = 4LL * num_sms();
+    if (blocks < 1) blocks = 1;
+    init_ws_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(base),
+                                                      words, n);
+}
+
 void init_bad_slots(unsigned long long* red, int n, cudaStream_t st) {
     init_bad_slots_kernel<<<(n + 127) / 128, 128, 0, st>>>(red, n);
 }

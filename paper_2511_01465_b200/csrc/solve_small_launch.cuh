@@ -19,7 +19,8 @@ int launch_resident(SolveParams& p, cudaStream_t st) {
     using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
     auto kern = resident_solve_kernel<P, KIND, S, THREADS, ITEMS>;
     const size_t smem = sizeof(typename E::Shared);
-    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    if (int rc = kernel_occupancy((const void*)kern, THREADS, smem, &per_sm)) return rc;
     kern<<<(unsigned)p.B, THREADS, smem, st>>>(p);
     ODX_CUDA(cudaGetLastError());
     count_launch(1);
@@ -71,9 +72,8 @@ int launch_persistent(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st
     // "bad" slots (4th of each iteration's reduction quad) start at all-ones
     init_bad_slots(p.red, p.max_iters + 1, st);
     const size_t smem = sizeof(typename E::Shared);
-    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+    if (int rc = kernel_occupancy((const void*)kern, THREADS, smem, &per_sm)) return rc;
     if (per_sm < 1) return fail(ODX_ECUDA, "persistent kernel cannot be resident");
     long long grid = (long long)per_sm * num_sms();
     if (grid > p.ntiles) grid = p.ntiles;
@@ -130,9 +130,8 @@ int launch_ws(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
     ODX_CUDA(cudaMemsetAsync(base + lay.zero_off, 0, lay.zero_bytes, st));
     init_bad_slots(wp.sp.red, p.max_iters + 1, st);
     const size_t smem = sizeof(typename W::Shared);
-    ODX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::NT, smem));
+    if (int rc = kernel_occupancy((const void*)kern, W::NT, smem, &per_sm)) return rc;
     if (per_sm < 1) return fail(ODX_ECUDA, "persistent kernel cannot be resident");
     long long grid = (long long)per_sm * num_sms();
     if (grid > lay.ntiles) grid = lay.ntiles;
@@ -158,9 +157,7 @@ int launch_grid_resident(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t
     const long long G = (p.N + E::T - 1) / E::T;
     const size_t smem = sizeof(typename E::Shared);
     int per_sm = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem) != cudaSuccess) {
+    if (kernel_occupancy((const void*)kern, THREADS, smem, &per_sm) != ODX_OK) {
         (void)cudaGetLastError();
         return ODX_EUNSUPPORTED;
     }
@@ -185,8 +182,7 @@ int launch_grid_resident(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t
     gp.sp.bar = reinterpret_cast<unsigned*>(base + o_bar);
     gp.halos = base + o_halo;
     gp.aggs = reinterpret_cast<double*>(base + o_aggs);
-    ODX_CUDA(cudaMemsetAsync(base, 0, zero_end, st));
-    init_bad_slots(gp.sp.red, p.max_iters + 1, st);
+    init_ws(base, zero_end, p.max_iters + 1, st);  // o_red == 0: the quads come first
     void* args[] = {&gp};
     ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(THREADS), args,
                                          smem, st));

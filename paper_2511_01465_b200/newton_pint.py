@@ -221,6 +221,25 @@ class _Buffers:
     def __init__(self):
         self.ws = {}
         self.pinned = {}
+        self.region = {}
+        self.wsq = {}
+
+    def device_region(self, dev, nbytes):
+        """Grow-only device scratch for host-in / host-out solves."""
+        import torch
+        buf = self.region.get(dev)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
+            self.region[dev] = buf
+        return buf
+
+    def ws_bytes(self, P, S, B, n, cfg):
+        key = (bytes(P), bytes(S), B, n, bytes(cfg))
+        v = self.wsq.get(key)
+        if v is None:
+            v = int(N.lib().odx_solve_workspace_bytes(P, S, B, n, cfg))
+            self.wsq[key] = v
+        return v
 
     def workspace(self, dev, nbytes):
         import torch
@@ -276,6 +295,33 @@ def solve_device(P, S, x0, X, dt: float, config: NewtonConfig, *, stream=None):
     N.check(L.odx_solve(P, S, N.ptr(x0), N.ptr(X), B, n, float(dt), cfg, base, base + o_sh,
                         base + o_it, base + o_st, base + o_sidx, N.ptr(ws), ws.numel(), st))
     return out
+
+
+def _solve_host(P, S, x0s: np.ndarray, X: np.ndarray, dt: float, config: NewtonConfig, dev):
+    """Host numpy in, host numpy out: one odx_solve_host call (one H2D, the
+    solve, one D2H through the library's cached pinned staging).
+    Returns (states (B, n, d), hist, shist, iters, status, sidx)."""
+    import torch
+    B, n, d = X.shape
+    H = config.max_iters + 1
+    x0c = np.ascontiguousarray(x0s, dtype=np.float64)
+    Xc = np.ascontiguousarray(X, dtype=np.float64)
+    # the result lands by DMA in page-locked memory from PyTorch's caching host
+    # allocator; the returned array is a view that keeps that block alive
+    states = torch.empty((B, n, d), dtype=torch.float64, pin_memory=True).numpy()
+    hist = np.empty((B, H), dtype=np.float64)
+    shist = np.empty((B, H), dtype=np.float64)
+    iters = np.empty(B, dtype=np.int32)
+    status = np.empty(B, dtype=np.int32)
+    sidx = np.empty(B, dtype=np.int64)
+    cfg = N.make_cfg(config.max_iters, config.residual_tol, config.step_tol,
+                     config.abort_on_nonfinite)
+    with torch.cuda.device(dev):
+        N.check(N.lib().odx_solve_host(
+            P, S, x0c.ctypes.data, Xc.ctypes.data, states.ctypes.data, B, n, float(dt), cfg,
+            hist.ctypes.data, shist.ctypes.data, iters.ctypes.data, status.ctypes.data,
+            sidx.ctypes.data, torch.cuda.current_stream(dev).cuda_stream))
+    return states, hist, shist, iters, status, sidx
 
 
 def _unpack_outcome(out_host: np.ndarray, B: int, H: int):
@@ -334,6 +380,12 @@ def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones
 
     t_begin = time.perf_counter()
     start = _resolve_guess(guess, problem, n, dt)
+    if output != "torch" and not _is_torch(start.states):
+        states, hist, shist, iters, status, sidx = _solve_host(
+            P, S, np.asarray(problem.x0, dtype=np.float64).reshape(1, -1),
+            np.asarray(start.states, dtype=np.float64).reshape(1, n, problem.dim), dt, config, dev)
+        return _report(problem, config, dt, n, states[0], hist, shist, iters, status, sidx,
+                       t_begin)
     if _is_torch(start.states):
         X = start.states.detach().to(device=dev, dtype=torch.float64).clone().contiguous()
     else:
@@ -346,6 +398,11 @@ def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones
     states_h = None if output == "torch" else _fetch(X[0], ("Xo", dev))
     torch.cuda.current_stream(dev).synchronize()
     hist, shist, iters, status, sidx = _unpack_outcome(out_h.numpy(), 1, H)
+    states = X[0] if output == "torch" else states_h.numpy().copy()
+    return _report(problem, config, dt, n, states, hist, shist, iters, status, sidx, t_begin)
+
+
+def _report(problem, config, dt, n, states, hist, shist, iters, status, sidx, t_begin):
     it_run, st, idx = int(iters[0]), int(status[0]), int(sidx[0])
     if st == N.ST_SINGULAR:
         raise SingularDiagonalBlockError(idx)
@@ -355,7 +412,6 @@ def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones
         raise RuntimeError("device solve did not report a status")
     h = hist[0, : it_run + 1]
     sh = shist[0, : it_run + 1]
-    states = X[0] if output == "torch" else states_h.numpy().copy()
     wall = time.perf_counter() - t_begin
     traj = Trajectory(problem.x0.copy(), states, dt, n)
     rec = config.record_residuals
@@ -383,6 +439,21 @@ def solve_batch(problem: OdeProblem, stepper: StepperIncrement, dt: float, x0s, 
     n = n_steps_for(problem, dt)
     dev = _device(device)
     t_begin = time.perf_counter()
+    if (output != "torch" and not _is_torch(x0s) and guess is not None
+            and not isinstance(guess, str) and not _is_torch(guess)):
+        x0h = np.ascontiguousarray(x0s, dtype=np.float64)
+        if x0h.ndim != 2 or x0h.shape[1] != problem.dim:
+            raise ValueError(f"x0s has shape {x0h.shape}, expected (B, {problem.dim})")
+        gh = np.asarray(guess, dtype=np.float64)
+        B = x0h.shape[0]
+        if gh.shape != (B, n, problem.dim):
+            raise ValueError(f"guess has shape {gh.shape}, expected {(B, n, problem.dim)}")
+        states, hist, shist, iters, status, sidx = _solve_host(P, S, x0h, gh, dt, config, dev)
+        rep = BatchSolveReport(states=states, residual_history=hist,
+                               scaled_residual_history=shist, iterations_run=iters,
+                               status=status, status_index=sidx, wall_time=0.0)
+        rep.wall_time = time.perf_counter() - t_begin
+        return rep
     x0t = (x0s.detach().to(dev, torch.float64).contiguous() if _is_torch(x0s)
            else _to_device(np.asarray(x0s), dev, ("x0", dev)))
     B, d = x0t.shape
