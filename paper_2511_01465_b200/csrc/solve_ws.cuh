@@ -617,7 +617,10 @@ persistent_ws_kernel(const WsParams wp) {
                 return r < 0 ? sm.xh[b][j] : sm.xr[b][r * D + j];
             };
             // apply tile (buffer c, first step `base`, its X rows in xk)
-            auto apply_tile = [&](int c, long long base, const double (&xk)[ITEMS][D]) {
+            // the old rows are re-read from L2 (read-only this iteration, loaded
+            // by this CTA a few microseconds ago) rather than kept in registers
+            // across the next tile's build
+            auto apply_tile = [&](int c, long long base) {
                 named_sync2<BAR_PREF, NT>(c);
                 if (tid == 0) TRACE(it, base / T, 4, gtime());
                 if (!do_scan) return;
@@ -661,7 +664,7 @@ persistent_ws_kernel(const WsParams wp) {
 #pragma unroll
                         for (int k = 0; k < D; k++) {
                             z[k] = dx[k];
-                            xn[i * D + k] = xk[i][k] + dx[k];
+                            xn[i * D + k] = __ldcg(cur + (base + r) * D + k) + dx[k];
                         }
                     }
                 }
@@ -680,7 +683,6 @@ persistent_ws_kernel(const WsParams wp) {
                 }
                 if (tid == 0) TRACE(it, base / T, 5, gtime());
             };
-            double xkp[ITEMS][D];
             long long basep = 0;
             int i = 0;
             for (;; i++) {
@@ -696,44 +698,43 @@ persistent_ws_kernel(const WsParams wp) {
                 if (t < 0) break;
                 if (tid == 0) TRACE(it, t, 0, gtime());
                 const long long base = t * T;
-                Elem<D> el[ITEMS];
-                double xkc[ITEMS][D];
+                // each item's element goes to shared memory (for the apply) and
+                // into the thread's running fold as soon as it is built, so no
+                // per-item element stays live in registers
+                Elem<D> agg;
+                bool has = false;
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++) {
                     const int r = tid * ITEMS + q;
                     const long long k = base + r;
                     if (k < N) {
-                        double prev[D], h[D];
+                        double prev[D], xk[D], h[D];
 #pragma unroll
                         for (int j = 0; j < D; j++) {
                             prev[j] = row(b, r - 1, j);
-                            xkc[q][j] = row(b, r, j);
+                            xk[j] = row(b, r, j);
                         }
-                        bool sing = build_step<P, KIND, S>(prob, p.sc, prev, xkc[q], k == 0, el[q], h);
+                        Elem<D> e;
+                        bool sing = build_step<P, KIND, S>(prob, p.sc, prev, xk, k == 0, e, h);
                         rn = nan_drop_max(rn, row_max_abs<D>(h));
-                        if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(el[q].c));
+                        if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
                         if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
-                    }
-                }
-                if (do_scan) {
-                    Elem<D> agg;
-                    bool has = false;
-#pragma unroll
-                    for (int q = 0; q < ITEMS; q++) {
-                        if (base + tid * ITEMS + q < N) {
+                        if (do_scan) {
                             double* dst = &sm.els[b][tid * EST + q * E];
 #pragma unroll
-                            for (int k = 0; k < D * D; k++) dst[k] = el[q].F[k];
+                            for (int kk = 0; kk < D * D; kk++) dst[kk] = e.F[kk];
 #pragma unroll
-                            for (int k = 0; k < D; k++) dst[D * D + k] = el[q].c[k];
+                            for (int kk = 0; kk < D; kk++) dst[D * D + kk] = e.c[kk];
                             if (has)
-                                compose<D>(agg, el[q], agg);
+                                compose<D>(agg, e, agg);
                             else {
-                                agg = el[q];
+                                agg = e;
                                 has = true;
                             }
                         }
                     }
+                }
+                if (do_scan) {
                     if (!has) set_identity<D>(agg);
                     warp_inclusive_scan<D>(agg, has, lane);
                     double* dst = &sm.tin[b][tid * AGS];
@@ -790,14 +791,10 @@ persistent_ws_kernel(const WsParams wp) {
                     }
                 }
                 named_arrive2<BAR_AGG, NT>(b);
-                if (i > 0) apply_tile(b ^ 1, basep, xkp);
-#pragma unroll
-                for (int q = 0; q < ITEMS; q++)
-#pragma unroll
-                    for (int j = 0; j < D; j++) xkp[q][j] = xkc[q][j];
+                if (i > 0) apply_tile(b ^ 1, basep);
                 basep = base;
             }
-            if (i > 0) apply_tile((i - 1) & 1, basep, xkp);
+            if (i > 0) apply_tile((i - 1) & 1, basep);
             if (tid == 0) {
                 tma_store_wait_all();
                 fence_proxy_async_global();
