@@ -104,108 +104,6 @@ __device__ __forceinline__ uint32_t lb_wait(const uint32_t* flags, long long j, 
     return f & 3u;
 }
 
-// Decoupled look-back for tile t (called by all 32 lanes of ONE warp).
-// A = this tile's aggregate (valid in lane 0).  Publishes AGG, walks back until
-// an inclusive prefix is found, returns the exclusive prefix state z (lane 0),
-// then publishes this tile's inclusive prefix A(z).
-template <int D>
-__device__ __forceinline__ void lookback_vec(long long t, uint32_t epoch, const Elem<D>& A,
-                                             bool A_has, uint32_t* flags, double* aggbuf,
-                                             double* inclbuf, double* z, int lane) {
-    constexpr int E = D * D + D;
-    if (t == 0) {
-        if (lane == 0) {
-#pragma unroll
-            for (int r = 0; r < D; r++) z[r] = 0.0;
-            double incl[D];
-            if (A_has)
-                apply<D>(A, z, incl);
-            else {
-#pragma unroll
-                for (int r = 0; r < D; r++) incl[r] = 0.0;
-            }
-#pragma unroll
-            for (int r = 0; r < D; r++) inclbuf[r] = incl[r];
-            st_release_u32(flags, lb_flag(epoch, LB_INCL));
-        }
-        __syncwarp();
-        return;
-    }
-    if (lane == 0) {
-        double* dst = aggbuf + t * E;
-        if (A_has) {
-#pragma unroll
-            for (int i = 0; i < D * D; i++) dst[i] = A.F[i];
-#pragma unroll
-            for (int i = 0; i < D; i++) dst[D * D + i] = A.c[i];
-        } else {
-            // a tile past the end carries the identity (never read by valid tiles)
-#pragma unroll
-            for (int r = 0; r < D; r++) {
-#pragma unroll
-                for (int s = 0; s < D; s++) dst[r * D + s] = (r == s) ? 1.0 : 0.0;
-                dst[D * D + r] = 0.0;
-            }
-        }
-        st_release_u32(flags + t, lb_flag(epoch, LB_AGG));
-    }
-    Elem<D> R;
-    bool R_has = false;
-    long long pos = t - 1;
-    while (true) {
-        long long j = pos - lane;
-        uint32_t kind = (j >= 0) ? lb_wait(flags, j, epoch) : LB_INCL;
-        unsigned incl_mask = __ballot_sync(FULL, kind == LB_INCL);
-        int first = incl_mask ? (__ffs(incl_mask) - 1) : 32;
-        Elem<D> e;
-        bool has = false;
-        if (lane < first) {
-            const double* src = aggbuf + j * E;
-#pragma unroll
-            for (int i = 0; i < D * D; i++) e.F[i] = __ldcg(src + i);
-#pragma unroll
-            for (int i = 0; i < D; i++) e.c[i] = __ldcg(src + D * D + i);
-            has = true;
-        } else if (lane == first) {
-#pragma unroll
-            for (int i = 0; i < D * D; i++) e.F[i] = 0.0;
-#pragma unroll
-            for (int i = 0; i < D; i++) e.c[i] = __ldcg(inclbuf + j * D + i);
-            has = true;
-        } else {
-#pragma unroll
-            for (int i = 0; i < D * D; i++) e.F[i] = 0.0;
-#pragma unroll
-            for (int i = 0; i < D; i++) e.c[i] = 0.0;
-        }
-        warp_reduce_latest_first<D>(e, has, lane);
-        if (lane == 0 && has) {
-            if (R_has)
-                compose<D>(e, R, R);  // e is earlier than what R already holds
-            else {
-                R = e;
-                R_has = true;
-            }
-        }
-        if (first < 32) break;
-        pos -= 32;
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int r = 0; r < D; r++) z[r] = R.c[r];
-        double incl[D];
-        if (A_has)
-            apply<D>(A, z, incl);
-        else {
-#pragma unroll
-            for (int r = 0; r < D; r++) incl[r] = z[r];
-        }
-#pragma unroll
-        for (int r = 0; r < D; r++) inclbuf[t * D + r] = incl[r];
-        st_release_u32(flags + t, lb_flag(epoch, LB_INCL));
-    }
-    __syncwarp();
-}
 
 // ---- block-wide reductions ---------------------------------------------------
 __device__ __forceinline__ double warp_max_nan_drop(double v) {

@@ -12,10 +12,12 @@
 //  * resident_solve_kernel — one CTA per trajectory (N <= THREADS*ITEMS), the
 //    whole solve in one launch with X resident in shared memory (BASELINE
 //    cfg 1 and the batched cfg 3).
-//  * persistent_solve_kernel — cooperative persistent grid for one long
-//    trajectory (cfg 2, cfg 5), tiles claimed in order from a per-iteration
-//    counter, X ping-ponged in HBM, a grid barrier and an identical
-//    on-device decision in every CTA after each iteration.
+//  * grid_resident_kernel — one trajectory over a co-resident wave of CTAs
+//    (cfg 2): each CTA keeps its tile of X in shared memory for the whole
+//    solve; one grid barrier, one aggregate fold and an identical on-device
+//    decision per iteration.
+//  * persistent_ws_kernel (solve_ws.cuh) — the streaming kernel for
+//    trajectories larger than one wave (cfg 5).
 //
 // The decision sequence is solve()'s (newton_pint.py:373-394) plus the
 // BASELINE step rule, identical to oracle/odescan_oracle.c:orc_solve.
@@ -336,127 +338,6 @@ resident_solve_kernel(const SolveParams p) {
         p.iters[b] = dd.iters;
         p.status[b] = dd.status;
         p.sidx[b] = dd.index;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Persistent cooperative solve for one long trajectory.
-// ---------------------------------------------------------------------------
-template <class P, int KIND, int S, int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS)
-persistent_solve_kernel(const SolveParams p) {
-    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
-    constexpr int D = P::D;
-    constexpr int NW = E::NW;
-    constexpr int T = E::T;
-    using L = typename E::L;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    typename E::Shared& sm = *reinterpret_cast<typename E::Shared*>(smem_raw);
-
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const long long N = p.N;
-    const P prob(p.prob);
-    const unsigned nblocks = gridDim.x;
-    double* cur = p.X;
-    double* nxt = p.Xalt;
-    double step_prev = __longlong_as_double(0x7ff8000000000000ll);
-    Decision dd{0, -1, -1, 0};
-
-    for (int it = 0; it <= p.max_iters; it++) {
-        const bool do_scan = it < p.max_iters;
-        const uint32_t epoch = (uint32_t)it + 1u;
-        double rn = 0.0, scn = 0.0, step = 0.0;
-        unsigned long long bad = ~0ull;
-        while (true) {
-            if (tid == 0) sm.tile = (long long)atomicAdd(p.ctr + it, 1u);
-            __syncthreads();
-            const long long t = sm.tile;
-            if (t >= p.ntiles) break;
-            const long long base = t * T;
-            // stage rows base-1 .. base+T-1 (row 0 = halo / x0)
-            for (int i = tid; i < (T + 1) * D; i += THREADS) {
-                long long g = (base - 1) * D + i;  // linear index into X
-                double v;
-                if (g < 0)
-                    v = p.x0[i];
-                else if (g < N * D)
-                    v = __ldcg(cur + g);
-                else
-                    v = 0.0;
-                sm.xs[L::idx(i)] = v;
-            }
-            __syncthreads();
-            Elem<D> el[ITEMS];
-            E::build_items(prob, p.sc, sm, base, N, el, rn, scn, bad);
-            if (do_scan) {
-                Elem<D> agg;
-                bool has;
-                E::block_scan(sm, base, N, el, agg, has);
-                __syncthreads();
-                if (w == 0) {
-                    Elem<D> A;
-                    bool A_has = false;
-                    if (lane == 0) E::tile_aggregate(sm, A, A_has);
-                    lookback_vec<D>(t, epoch, A, A_has, p.flags, p.aggbuf, p.inclbuf, sm.z, lane);
-                }
-                __syncthreads();
-                E::apply_items(sm, base, N, el, agg, has, step);
-                __syncthreads();
-                for (int i = tid; i < T * D; i += THREADS) {
-                    long long g = base * D + i;
-                    if (g < N * D) nxt[g] = sm.xs[L::idx(i + D)];
-                }
-            }
-            __syncthreads();
-        }
-        // per-block reductions -> one atomic each
-        rn = warp_max_nan_drop(rn);
-        scn = warp_max_nan_drop(scn);
-        step = warp_max_nan_drop(step);
-        bad = warp_min_u64(bad);
-        if (lane == 0) {
-            sm.redd[0][w] = rn; sm.redd[1][w] = scn; sm.redd[2][w] = step; sm.redb[w] = bad;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            double a = 0.0, c = 0.0, s = 0.0;
-            unsigned long long m = ~0ull;
-            for (int q = 0; q < NW; q++) {
-                a = fmax(a, sm.redd[0][q]);
-                c = fmax(c, sm.redd[1][q]);
-                s = fmax(s, sm.redd[2][q]);
-                m = sm.redb[q] < m ? sm.redb[q] : m;
-            }
-            unsigned long long* red = p.red + 4ll * it;
-            if (a > 0.0) atomicMax(red + 0, dbits(a));
-            if (c > 0.0) atomicMax(red + 1, dbits(c));
-            if (s > 0.0) atomicMax(red + 2, dbits(s));
-            if (m != ~0ull) atomicMin(red + 3, m);
-        }
-        grid_barrier(p.bar, p.bar + 1, nblocks);
-        const unsigned long long* red = p.red + 4ll * it;
-        const double rnb = bitsd(__ldcg(red + 0));
-        const double scb = (KIND == 0) ? rnb : bitsd(__ldcg(red + 1));
-        const unsigned long long badb = __ldcg(red + 3);
-        dd = decide(it, p, rnb, badb, step_prev);
-        if (blockIdx.x == 0 && tid == 0 && dd.status != ODX_ST_SINGULAR) {
-            if (p.hist) p.hist[it] = rnb;
-            if (p.shist) p.shist[it] = scb;
-        }
-        if (dd.stop) break;
-        step_prev = bitsd(__ldcg(red + 2));
-        double* t2 = cur; cur = nxt; nxt = t2;
-    }
-    if (cur != p.X) {
-        const long long total = N * D;
-        for (long long i = (long long)blockIdx.x * THREADS + tid; i < total;
-             i += (long long)nblocks * THREADS)
-            p.X[i] = __ldcg(cur + i);
-    }
-    if (blockIdx.x == 0 && tid == 0) {
-        p.iters[0] = dd.iters;
-        p.status[0] = dd.status;
-        p.sidx[0] = dd.index;
     }
 }
 

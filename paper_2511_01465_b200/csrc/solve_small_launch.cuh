@@ -27,71 +27,10 @@ int launch_resident(SolveParams& p, cudaStream_t st) {
     return ODX_OK;
 }
 
-// Workspace of the persistent solve: X ping-pong buffer, look-back flags and
-// payloads, per-iteration tile counters / reductions, grid-barrier words.
-template <int D>
-struct PersistLayout {
-    size_t total = 0, zero_off = 0, zero_bytes = 0;
-    size_t Xalt, flags, ctr, red, bar, aggbuf, inclbuf;
-    long long ntiles = 0;
-    PersistLayout(long long N, long long T, int max_iters) {
-        ntiles = (N + T - 1) / T;
-        Carver c{nullptr};
-        auto at = [&](size_t bytes) { c.off = align_up(c.off, 256); size_t o = c.off; c.off += bytes; return o; };
-        Xalt = at((size_t)N * D * sizeof(double));
-        zero_off = align_up(c.off, 256);
-        flags = at((size_t)ntiles * 4);
-        ctr = at(((size_t)max_iters + 1) * 4);
-        red = at(4 * ((size_t)max_iters + 1) * 8);
-        bar = at(2 * 4);
-        zero_bytes = c.off - zero_off;
-        aggbuf = at((size_t)ntiles * (D * D + D) * sizeof(double));
-        inclbuf = at((size_t)ntiles * D * sizeof(double));
-        total = c.off + 256;  // + alignment slack of the caller's base pointer
-    }
-};
-
-template <class P, int KIND, int S, int THREADS, int ITEMS>
-int launch_persistent(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
-    using E = SmallEngine<P, KIND, S, THREADS, ITEMS>;
-    constexpr int D = P::D;
-    auto kern = persistent_solve_kernel<P, KIND, S, THREADS, ITEMS>;
-    const PersistLayout<D> lay(p.N, (long long)THREADS * ITEMS, p.max_iters);
-    if (ws == nullptr || ws_bytes < lay.total)
-        return fail(ODX_EWORKSPACE, "workspace too small for persistent solve");
-    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
-    p.Xalt = reinterpret_cast<double*>(base + lay.Xalt);
-    p.flags = reinterpret_cast<uint32_t*>(base + lay.flags);
-    p.ctr = reinterpret_cast<uint32_t*>(base + lay.ctr);
-    p.red = reinterpret_cast<unsigned long long*>(base + lay.red);
-    p.bar = reinterpret_cast<unsigned*>(base + lay.bar);
-    p.aggbuf = reinterpret_cast<double*>(base + lay.aggbuf);
-    p.inclbuf = reinterpret_cast<double*>(base + lay.inclbuf);
-    p.ntiles = lay.ntiles;
-    ODX_CUDA(cudaMemsetAsync(base + lay.zero_off, 0, lay.zero_bytes, st));
-    // "bad" slots (4th of each iteration's reduction quad) start at all-ones
-    init_bad_slots(p.red, p.max_iters + 1, st);
-    const size_t smem = sizeof(typename E::Shared);
-    int per_sm = 0;
-    if (int rc = kernel_occupancy((const void*)kern, THREADS, smem, &per_sm)) return rc;
-    if (per_sm < 1) return fail(ODX_ECUDA, "persistent kernel cannot be resident");
-    long long grid = (long long)per_sm * num_sms();
-    if (grid > p.ntiles) grid = p.ntiles;
-    void* args[] = {&p};
-    ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(THREADS),
-                                         args, smem, st));
-    ODX_CUDA(cudaGetLastError());
-    count_launch(2);  // init_bad_slots + the persistent solve
-    return ODX_OK;
-}
-
-// Workspace of the warp-specialised solve: X ping-pong buffer, look-back
-// records (zeroed: tag 0 never matches an epoch), tile counters, reductions,
-// grid-barrier words.
 template <int D>
 struct WsLayout {
     size_t total = 0, zero_off = 0, zero_bytes = 0;
-    size_t Xalt, recs, gsums, ctr, red, bar;
+    size_t Xalt, recs, ctr, red, bar;
     long long ntiles = 0;
     WsLayout(long long N, long long T, int max_iters) {
         ntiles = (N + T - 1) / T;
@@ -100,7 +39,6 @@ struct WsLayout {
         Xalt = at((size_t)N * D * sizeof(double));
         zero_off = align_up(off, 256);
         recs = at((size_t)ntiles * sizeof(LbRecord<D>));
-        gsums = at((size_t)((ntiles + 31) / 32 + 1) * (D * D + D) * sizeof(Chunk));
         ctr = at(((size_t)max_iters + 1) * 4);
         red = at(4 * ((size_t)max_iters + 1) * 8);
         bar = at(2 * 4);
@@ -126,7 +64,6 @@ int launch_ws(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
     wp.sp.bar = reinterpret_cast<unsigned*>(base + lay.bar);
     wp.sp.ntiles = lay.ntiles;
     wp.recs = base + lay.recs;
-    wp.gsums = base + lay.gsums;
     ODX_CUDA(cudaMemsetAsync(base + lay.zero_off, 0, lay.zero_bytes, st));
     init_bad_slots(wp.sp.red, p.max_iters + 1, st);
     const size_t smem = sizeof(typename W::Shared);
@@ -199,13 +136,6 @@ inline bool use_grid_resident() {
     return on;
 }
 
-inline bool use_legacy_persistent() {
-    static const bool legacy = [] {
-        const char* v = std::getenv("ODX_PERSISTENT");
-        return v && std::strcmp(v, "legacy") == 0;
-    }();
-    return legacy;
-}
 
 // items per compute thread of the warp-specialised kernel, by state dim
 template <int D>
@@ -213,13 +143,14 @@ constexpr int ws_items() { return D == 1 ? 8 : (D == 2 ? 4 : 2); }
 
 }  // namespace
 
-// Resident path when the whole trajectory fits one CTA; persistent otherwise.
+// Resident path when the whole trajectory fits one CTA; grid-resident when one
+// trajectory fits a co-resident wave of CTAs; the streaming warp-specialised
+// kernel otherwise.
 template <class P, int KIND, int S>
 int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
                 size_t* need) {
     constexpr int D = P::D;
     constexpr int RI = (D <= 3) ? 8 : 4;   // items per thread, resident
-    constexpr int PI = (D <= 2) ? 4 : 2;   // items per thread, persistent
     const bool resident = p.N <= 256LL * RI;
     constexpr int WI = ws_items<D>();
     const bool small_ws = p.N < 128LL * WI * 296;  // keep >= 2 tiles per SM
@@ -239,13 +170,8 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
     if (query) {
         *need = 0;
         if (!resident) {
-            if (use_legacy_persistent()) {
-                const long long T = (p.N < 128LL * PI * 296) ? 128 : 128LL * PI;
-                *need = PersistLayout<D>(p.N, T, p.max_iters).total;
-            } else {
-                const long long T = small_ws ? 128 : 128LL * WI;
-                *need = WsLayout<D>(p.N, T, p.max_iters).total;
-            }
+            const long long T = small_ws ? 128 : 128LL * WI;
+            *need = WsLayout<D>(p.N, T, p.max_iters).total;
         }
         return ODX_OK;
     }
@@ -254,11 +180,6 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
         return launch_resident<P, KIND, S, 256, RI>(p, st);
     }
     if (p.B != 1) return fail(ODX_EUNSUPPORTED, "batched solve needs N <= resident limit");
-    if (use_legacy_persistent()) {
-        // small N: 1 item/thread keeps >= 2 tiles per SM; large N: PI items/thread
-        if (p.N < 128LL * PI * 296) return launch_persistent<P, KIND, S, 128, 1>(p, ws, ws_bytes, st);
-        return launch_persistent<P, KIND, S, 128, PI>(p, ws, ws_bytes, st);
-    }
     if (small_ws) return launch_ws<P, KIND, S, 4, 1>(p, ws, ws_bytes, st);
     return launch_ws<P, KIND, S, 4, WI>(p, ws, ws_bytes, st);
 }

@@ -70,231 +70,14 @@ struct LbRecord<D, false> {
 struct WsParams {
     SolveParams sp;
     void* recs;   // LbRecord<D>[ntiles]
-    void* gsums;  // Chunk[nblocks32][D*D+D]: aggregates of aligned 32-tile blocks
 };
 
-// Poll one look-back record until it is usable in this epoch.  want_agg:
-// also require the AGG payload (block-boundary tiles need every aggregate).
-// Returns 2 if the inclusive prefix is valid (e = (0, prefix)), else 1 with
-// e = the tile aggregate.
-template <int D>
-__device__ __forceinline__ int lb_poll(const LbRecord<D>* rec, unsigned long long tagA,
-                                       unsigned long long tagI, bool want_agg, Elem<D>& e,
-                                       Elem<D>& aggv) {
-    // Poll only the first chunk of each payload (cheap on L2); fetch the rest
-    // once a tag matches and re-verify every chunk (self-validating records).
-    unsigned sleep_ns = 32;  // spin count (short sleeps after a few polls)
-    while (true) {
-        const Chunk i0 = ld_chunk(&rec->incl[0]);
-        const Chunk a0 = ld_chunk(&rec->agg[0]);
-        const bool iv0 = (i0.tag == tagI), av0 = (a0.tag == tagA);
-        if (av0 || (iv0 && !want_agg)) {
-            bool iv = iv0, av = av0;
-            double ci[D];
-            ci[0] = i0.v;
-#pragma unroll
-            for (int k = 1; k < D; k++) {
-                Chunk ch = ld_chunk(&rec->incl[k]);
-                ci[k] = ch.v;
-                iv &= (ch.tag == tagI);
-            }
-            if (av0) {
-                aggv.F[0] = a0.v;
-#pragma unroll
-                for (int k = 1; k < D * D; k++) {
-                    Chunk ch = ld_chunk(&rec->agg[k]);
-                    aggv.F[k] = ch.v;
-                    av &= (ch.tag == tagA);
-                }
-#pragma unroll
-                for (int k = 0; k < D; k++) {
-                    Chunk ch = ld_chunk(&rec->agg[D * D + k]);
-                    aggv.c[k] = ch.v;
-                    av &= (ch.tag == tagA);
-                }
-            }
-            if (iv && (av || !want_agg)) {
-#pragma unroll
-                for (int k = 0; k < D * D; k++) e.F[k] = 0.0;
-#pragma unroll
-                for (int k = 0; k < D; k++) e.c[k] = ci[k];
-                return 2;
-            }
-            if (av) {
-                e = aggv;
-                return 1;
-            }
-        }
-        if (++sleep_ns > 40) __nanosleep(16);
-    }
-}
-
-// Two-level decoupled look-back for tile t (all 32 lanes of the control warp).
-// Level 1 walks tile records (32 tiles per round); once past the most recent
-// 32 tiles it aligns to 32-tile blocks and walks block aggregates (1024 tiles
-// per round).  The first tile of every block publishes the previous block's
-// aggregate, so the inclusive-prefix frontier is never more than a couple of
-// rounds away.  Returns the exclusive prefix state in z (lane 0).
-template <int D, bool LEVEL2>
-__device__ __forceinline__ void lookback2(long long t, unsigned long long tagA,
-                                          unsigned long long tagI, unsigned long long tagG,
-                                          LbRecord<D>* recs, Chunk* gsums, double* z, int lane) {
-    constexpr int E = D * D + D;
-    Elem<D> R;
-    bool R_has = false;
-    auto fold = [&](Elem<D>& e, bool has) {
-        warp_reduce_latest_first<D>(e, has, lane);
-        if (lane == 0 && has) {
-            if (R_has)
-                compose<D>(e, R, R);
-            else {
-                R = e;
-                R_has = true;
-            }
-        }
-    };
-    auto sentinel = [&](Elem<D>& e) {  // the state before tile 0 is the zero offset
-#pragma unroll
-        for (int k = 0; k < D * D; k++) e.F[k] = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; k++) e.c[k] = 0.0;
-    };
-    // ---- round 1: tiles t-1 .. t-32 --------------------------------------
-    const bool block_start = LEVEL2 && (t % 32 == 0);
-    {
-        const long long j = t - 1 - lane;
-        Elem<D> e, av;
-        int kind = 2;
-        if (j >= 0)
-            kind = lb_poll<D>(&recs[j], tagA, tagI, block_start, e, av);
-        else
-            sentinel(e);
-        if (block_start) {
-            // publish the aggregate of block t/32 - 1 (tiles t-32 .. t-1)
-            Elem<D> g = av;
-            bool gh = true;
-            warp_reduce_latest_first<D>(g, gh, lane);
-            if (lane == 0) {
-                Chunk* dst = gsums + (t / 32 - 1) * E;
-#pragma unroll
-                for (int k = 0; k < D * D; k++) st_chunk(dst + k, g.F[k], tagG);
-#pragma unroll
-                for (int k = 0; k < D; k++) st_chunk(dst + D * D + k, g.c[k], tagG);
-            }
-        }
-        const unsigned m = __ballot_sync(FULL, kind == 2);
-        const int first = m ? (__ffs(m) - 1) : 32;
-        fold(e, lane <= first);
-        if (first < 32) goto done;
-    }
-    if (!LEVEL2) {
-        // plain decoupled look-back: 32 tiles per round
-        long long pos = t - 33;
-        while (true) {
-            const long long j = pos - lane;
-            Elem<D> e, av;
-            int kind = 2;
-            if (j >= 0)
-                kind = lb_poll<D>(&recs[j], tagA, tagI, false, e, av);
-            else
-                sentinel(e);
-            const unsigned m = __ballot_sync(FULL, kind == 2);
-            const int first = m ? (__ffs(m) - 1) : 32;
-            fold(e, lane <= first);
-            if (first < 32) goto done;
-            pos -= 32;
-        }
-    }
-    {
-        long long q = t - 33;  // newest tile not yet folded (q >= 0 here)
-        // ---- partial round up to the block boundary -----------------------
-        if ((q & 31) != 31) {
-            const int n = (int)(q & 31) + 1;
-            const long long j = q - lane;
-            Elem<D> e, av;
-            int kind = 2;
-            if (lane < n)
-                kind = lb_poll<D>(&recs[j], tagA, tagI, false, e, av);
-            else
-                sentinel(e);
-            const unsigned m = __ballot_sync(FULL, kind == 2 && lane < n);
-            const int first = m ? (__ffs(m) - 1) : 32;
-            fold(e, lane <= first && lane < n);
-            if (first < 32) goto done;
-            q -= n;
-        }
-        // ---- level 2: whole blocks ending at q (q = 32k + 31) -------------
-        while (true) {
-            const long long kb = (q + 1) / 32 - 1 - lane;  // block of this lane
-            Elem<D> e;
-            int kind = 2;
-            if (kb >= 0) {
-                const long long last = kb * 32 + 31;
-                const Chunk* g = gsums + kb * E;
-                int spins = 0;
-                while (true) {
-                    bool iv = true, gv = true;
-                    double ci[D];
-#pragma unroll
-                    for (int k = 0; k < D; k++) {
-                        Chunk ch = ld_chunk(&recs[last].incl[k]);
-                        ci[k] = ch.v;
-                        iv &= (ch.tag == tagI);
-                    }
-                    if (iv) {
-#pragma unroll
-                        for (int k = 0; k < D * D; k++) e.F[k] = 0.0;
-#pragma unroll
-                        for (int k = 0; k < D; k++) e.c[k] = ci[k];
-                        kind = 2;
-                        break;
-                    }
-#pragma unroll
-                    for (int k = 0; k < E; k++) {
-                        Chunk ch = ld_chunk(g + k);
-                        if (k < D * D)
-                            e.F[k] = ch.v;
-                        else
-                            e.c[k - D * D] = ch.v;
-                        gv &= (ch.tag == tagG);
-                    }
-                    if (gv) {
-                        kind = 1;
-                        break;
-                    }
-                    if (++spins > 4) __nanosleep(20);
-                }
-            } else {
-                sentinel(e);
-            }
-            const unsigned m = __ballot_sync(FULL, kind == 2);
-            const int first = m ? (__ffs(m) - 1) : 32;
-            fold(e, lane <= first);
-            if (first < 32) break;
-            q -= 32 * 32;
-        }
-    }
-done:
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < D; k++) z[k] = R.c[k];
-    }
-}
-
-// Wide decoupled look-back, one L2 round trip per round: each lane covers LBK
-// consecutive tiles (a round examines 32*LBK tiles); all their record chunks
-// ({value, tag}, 16 B) are staged into the lane's shared-memory area with one
-// batch of cp.async, then validated from smem (self-validating tags) — tiles
-// not yet published are re-fetched.  Returns the exclusive prefix state (lane 0).
+// Wide decoupled look-back: each lane covers LBK consecutive tiles (a round
+// examines 32*LBK tiles).  The round's records ({value, tag} chunks, 16 B) are
+// staged into shared memory by one TMA bulk copy, then validated from smem
+// (self-validating tags); a round with unpublished tiles is fetched again.
+// Returns the exclusive prefix state (lane 0).
 constexpr int LBK = 5;  // odd: see LbRecord
-
-__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 
 template <int D>
 __device__ __forceinline__ void lookback_wide1(long long t, unsigned long long tagA,
@@ -473,7 +256,6 @@ persistent_ws_kernel(const WsParams wp) {
 
     const SolveParams& p = wp.sp;
     Rec* recs = reinterpret_cast<Rec*>(wp.recs);
-    Chunk* gsums = reinterpret_cast<Chunk*>(wp.gsums);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const bool is_ctl = (w == NCW);
     const long long N = p.N;
@@ -498,7 +280,6 @@ persistent_ws_kernel(const WsParams wp) {
         const bool do_scan = it < p.max_iters;
         const uint32_t epoch = (uint32_t)it + 1u;
         const unsigned long long tagA = lb_tag(epoch, 1), tagI = lb_tag(epoch, 2);
-        const unsigned long long tagG = lb_tag(epoch, 3);
 
         if (is_ctl) {
             // ------------------------------------------------ control warp --
