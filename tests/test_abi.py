@@ -77,3 +77,29 @@ def test_invalid_arguments_fail_without_launch():
     assert rc == N.ODX_EINVAL
     with pytest.raises(ValueError):
         N.check(N.ODX_EINVAL)
+
+
+def test_solve_host_validates_before_any_device_work():
+    """odx_solve_host rejects null host buffers and empty shapes with
+    ODX_EINVAL and a message, before touching CUDA (runs without a GPU)."""
+    import numpy as np
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200 import _native as N
+    L = N.lib()
+    p = pkg.van_der_pol()
+    s = pkg.get_stepper("rk4", p)
+    cfg = N.make_cfg(3, 0.0, 0.0, True)
+    x0 = np.zeros(2)
+    X = np.zeros((8, 2))
+    out = np.zeros((8, 2))
+    it = np.zeros(1, np.int32)
+    st = np.zeros(1, np.int32)
+    ix = np.zeros(1, np.int64)
+    rc = L.odx_solve_host(p.native(), s.native(), x0.ctypes.data, None, out.ctypes.data, 1, 8,
+                          1e-3, cfg, None, None, it.ctypes.data, st.ctypes.data, ix.ctypes.data,
+                          None)
+    assert rc == N.ODX_EINVAL and b"null" in L.odx_last_error()
+    rc = L.odx_solve_host(p.native(), s.native(), x0.ctypes.data, X.ctypes.data, out.ctypes.data,
+                          1, 0, 1e-3, cfg, None, None, it.ctypes.data, st.ctypes.data,
+                          ix.ctypes.data, None)
+    assert rc == N.ODX_EINVAL

@@ -422,3 +422,38 @@ def test_cfg4_full_size_first_iterates(pkg, oracle):
     assert np.isfinite(r.states[0]).all()
     h = r.residual_history[0]
     assert np.isfinite(h).all() and h[100] < h[5]  # the late phase contracts (A.2)
+
+
+def test_host_buffer_path_matches_device_path(pkg):
+    """odx_solve_host (numpy in / numpy out: what solve() and solve_batch()
+    use for host arrays) against the device-buffer path on the same inputs:
+    identical iterates, histories (NaN past the iterations run), statuses —
+    for pageable and for page-locked (DMA'd directly) guesses."""
+    import torch
+    from paper_2511_01465_b200.configs import CONFIGS
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    cfg = CONFIGS[2]
+    n = 4096
+    prob = _cfg_problem(pkg, cfg)
+    prob = type(prob)(**{**prob.__dict__, "tf": n * cfg.dt})
+    st = pkg.get_stepper(cfg.stepper, prob)
+    x0s = cfg.x0s()
+    guess = np.broadcast_to(x0s[:, None, :], (1, n, 2)).copy()
+    pinned = torch.empty((1, n, 2), dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[:] = guess
+    for conf in (pkg.NewtonConfig(max_iters=4, step_tol=0.0, abort_on_nonfinite=False),
+                 pkg.NewtonConfig(max_iters=6, abort_on_nonfinite=True)):
+        dev = solve_batch(prob, st, cfg.dt, x0s, torch.from_numpy(guess).cuda(), conf)
+        for g in (guess, pinned.numpy()):
+            host = solve_batch(prob, st, cfg.dt, x0s, g, conf)
+            assert isinstance(host.states, np.ndarray)
+            assert np.array_equal(host.states, np.asarray(dev.states), equal_nan=True)
+            assert np.array_equal(host.residual_history, dev.residual_history, equal_nan=True)
+            assert np.array_equal(host.scaled_residual_history, dev.scaled_residual_history,
+                                  equal_nan=True)
+            assert np.array_equal(host.status, dev.status)
+            assert np.array_equal(host.iterations_run, dev.iterations_run)
+            assert np.array_equal(host.status_index, dev.status_index)
+            it = int(host.iterations_run[0])
+            assert np.isnan(host.residual_history[0, it + 1:]).all()
+    assert np.array_equal(pinned.numpy(), guess)  # the guess is never written
