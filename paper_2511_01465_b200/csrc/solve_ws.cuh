@@ -245,7 +245,7 @@ __device__ __forceinline__ unsigned long long lb_tag(uint32_t epoch, uint32_t ki
 }
 
 template <class P, int KIND, int S, int NCW, int ITEMS>
-__global__ void __launch_bounds__((NCW + 1) * 32, 2)
+__global__ void __launch_bounds__((NCW + 1) * 32, (NCW <= 4) ? 2 : 1)
 persistent_ws_kernel(const WsParams wp) {
     using W = WsEngine<P, KIND, S, NCW, ITEMS>;
     constexpr int D = W::D, E = W::E, NCT = W::NCT, NT = W::NT, T = W::T;

@@ -34,7 +34,7 @@ int main(int argc, char** argv) {
         solve_small<VanDerPol, 0, 4>(q, nullptr, 0, 0, true, &ws_bytes);
     }
     void* ws; cudaMalloc(&ws, ws_bytes);
-    long long ntiles = (N + 511) / 512;
+    long long ntiles = (N + 255) / 256;
     unsigned long long* tr; cudaMalloc(&tr, ntiles * 128); cudaMemset(tr, 0, ntiles * 128);
     cudaMemcpyToSymbol(g_trace, &tr, sizeof(tr));
     for (int rep = 0; rep < 2; rep++) {
