@@ -137,9 +137,11 @@ inline bool use_grid_resident() {
 }
 
 
-#ifndef WS_NCW
-#define WS_NCW 8  // compute warps per CTA of the large-N streaming kernel (1 CTA/SM)
-#endif
+// compute warps per CTA of the large-N streaming kernel: d <= 2 runs 8 warps
+// x 1024-step tiles at one CTA per SM (half the look-backs of 512-step
+// tiles); larger d keeps 4 warps (its elements would not fit shared memory)
+template <int D>
+constexpr int ws_ncw() { return D <= 2 ? 8 : 4; }
 // items per compute thread of the warp-specialised kernel, by state dim
 template <int D>
 constexpr int ws_items() { return D == 1 ? 8 : (D == 2 ? 4 : 2); }
@@ -173,7 +175,7 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
     if (query) {
         *need = 0;
         if (!resident) {
-            const long long T = small_ws ? 128 : 32LL * WS_NCW * WI;
+            const long long T = small_ws ? 128 : 32LL * ws_ncw<D>() * WI;
             *need = WsLayout<D>(p.N, T, p.max_iters).total;
         }
         return ODX_OK;
@@ -184,7 +186,7 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
     }
     if (p.B != 1) return fail(ODX_EUNSUPPORTED, "batched solve needs N <= resident limit");
     if (small_ws) return launch_ws<P, KIND, S, 4, 1>(p, ws, ws_bytes, st);
-    return launch_ws<P, KIND, S, WS_NCW, WI>(p, ws, ws_bytes, st);
+    return launch_ws<P, KIND, S, ws_ncw<D>(), WI>(p, ws, ws_bytes, st);
 }
 
 }  // namespace odx
