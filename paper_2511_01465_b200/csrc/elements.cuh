@@ -170,6 +170,85 @@ __device__ __forceinline__ void build_explicit_step(const P& prob, const StepCoe
         }
 }
 
+// NI independent steps built together, stage by stage (the loops over items
+// are innermost), so the scheduler sees NI independent dependency chains at
+// every point of the RK stage sequence.  Same arithmetic, per item, as
+// build_explicit_step.
+template <class P, int S, int NI>
+__device__ __forceinline__ void build_explicit_multi(const P& prob, const StepCoefs& sc,
+                                                     const double (&prev)[NI][P::D],
+                                                     const double (&xk)[NI][P::D],
+                                                     const bool (&first)[NI], Elem<P::D> (&el)[NI],
+                                                     double (&h)[NI][P::D]) {
+    constexpr int D = P::D;
+    double kap[S][NI][D];
+    double dkap[S][NI][D * D];
+#pragma unroll
+    for (int i = 0; i < S; i++) {
+        double xs[NI][D];
+#pragma unroll
+        for (int n = 0; n < NI; n++)
+#pragma unroll
+            for (int r = 0; r < D; r++) {
+                double acc = prev[n][r];
+#pragma unroll
+                for (int j = 0; j < i; j++) acc += sc.dta[i * S + j] * kap[j][n][r];
+                xs[n][r] = acc;
+            }
+        double Js[NI][D * D];
+#pragma unroll
+        for (int n = 0; n < NI; n++) {
+            prob.f(xs[n], kap[i][n]);
+            prob.jac(xs[n], Js[n]);
+        }
+#pragma unroll
+        for (int n = 0; n < NI; n++) {
+            double M[D * D];
+#pragma unroll
+            for (int r = 0; r < D; r++)
+#pragma unroll
+                for (int c = 0; c < D; c++) {
+                    double m = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+                    for (int j = 0; j < i; j++) m += sc.dta[i * S + j] * dkap[j][n][r * D + c];
+                    M[r * D + c] = m;
+                }
+#pragma unroll
+            for (int r = 0; r < D; r++)
+#pragma unroll
+                for (int c = 0; c < D; c++) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < D; q++) acc += Js[n][r * D + q] * M[q * D + c];
+                    dkap[i][n][r * D + c] = acc;
+                }
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < NI; n++) {
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < S; i++) acc += sc.b[i] * kap[i][n][r];
+            const double g = sc.dt * acc;
+            const double hv = xk[n][r] - prev[n][r] - g;
+            h[n][r] = hv;
+            el[n].c[r] = -hv;
+        }
+#pragma unroll
+        for (int r = 0; r < D; r++)
+#pragma unroll
+            for (int c = 0; c < D; c++) {
+                double acc = 0.0;
+#pragma unroll
+                for (int i = 0; i < S; i++) acc += sc.b[i] * dkap[i][n][r * D + c];
+                const double jg = sc.dt * acc;
+                el[n].F[r * D + c] = first[n] ? 0.0 : jg + ((r == c) ? 1.0 : 0.0);
+            }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Register LU with partial pivoting (_kernels.py:28-77).  Row swaps are
 // expressed as predicated moves over compile-time indices so A stays in

@@ -137,11 +137,12 @@ inline bool use_grid_resident() {
 }
 
 
-// compute warps per CTA of the large-N streaming kernel: d <= 2 runs 8 warps
-// x 1024-step tiles at one CTA per SM (half the look-backs of 512-step
-// tiles); larger d keeps 4 warps (its elements would not fit shared memory)
+// compute warps per CTA of the large-N streaming kernel: d <= 2 runs 7 warps
+// x 896-step tiles at one CTA per SM (8 warps per SM leave 255 registers per
+// thread; fewer, larger tiles than 4-warp CTAs mean fewer look-backs); larger
+// d keeps 4 warps (its elements would not fit shared memory)
 template <int D>
-constexpr int ws_ncw() { return D <= 2 ? 8 : 4; }
+constexpr int ws_ncw() { return D <= 2 ? 7 : 4; }
 // items per compute thread of the warp-specialised kernel, by state dim
 template <int D>
 constexpr int ws_items() { return D == 1 ? 8 : (D == 2 ? 4 : 2); }

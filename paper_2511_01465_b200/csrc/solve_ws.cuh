@@ -78,6 +78,14 @@ struct WsParams {
 // (self-validating tags); a round with unpublished tiles is fetched again.
 // Returns the exclusive prefix state (lane 0).
 constexpr int LBK = 5;  // odd: see LbRecord
+// register budget per thread: a sub-partition (SMSP) holds 16K registers, so
+// 3 warps on one SMSP cap a thread at 168 and 2 warps at 255.  4 compute warps
+// + control run two CTAs per SM (10 warps: 168); 7 + control run one (8
+// warps: the build can keep two items' RK stages in flight without spilling)
+#define WS_MAXREG(ncw) ((ncw) <= 4 ? 168 : 255)
+#ifndef WS_PAIR
+#define WS_PAIR 2  // explicit steps built together per thread (see build_explicit_multi)
+#endif
 
 template <int D>
 __device__ __forceinline__ void lookback_wide1(long long t, unsigned long long tagA,
@@ -245,7 +253,7 @@ __device__ __forceinline__ unsigned long long lb_tag(uint32_t epoch, uint32_t ki
 }
 
 template <class P, int KIND, int S, int NCW, int ITEMS>
-__global__ void __launch_bounds__((NCW + 1) * 32, (NCW <= 4) ? 2 : 1)
+__global__ void __maxnreg__(WS_MAXREG(NCW))
 persistent_ws_kernel(const WsParams wp) {
     using W = WsEngine<P, KIND, S, NCW, ITEMS>;
     constexpr int D = W::D, E = W::E, NCT = W::NCT, NT = W::NT, T = W::T;
@@ -402,6 +410,25 @@ persistent_ws_kernel(const WsParams wp) {
             // by this CTA a few microseconds ago) rather than kept in registers
             // across the next tile's build
             auto apply_tile = [&](int c, long long base) {
+                // the old rows (L2) are requested before waiting for the prefix
+                double xold[ITEMS * D];
+                {
+                    const long long r0 = base + (long long)tid * ITEMS;
+                    const double* src = cur + r0 * D;
+                    if (do_scan && r0 + ITEMS <= N && ((ITEMS * D) & 1) == 0 &&
+                        (reinterpret_cast<size_t>(src) & 15) == 0) {
+#pragma unroll
+                        for (int q = 0; q < ITEMS * D; q += 2) {
+                            const double2 v = __ldcg(reinterpret_cast<const double2*>(src + q));
+                            xold[q] = v.x;
+                            xold[q + 1] = v.y;
+                        }
+                    } else if (do_scan) {
+#pragma unroll
+                        for (int q = 0; q < ITEMS * D; q++)
+                            xold[q] = (r0 * D + q < N * D) ? __ldcg(src + q) : 0.0;
+                    }
+                }
                 named_sync2<BAR_PREF, NT>(c);
                 if (tid == 0) TRACE(it, base / T, 4, gtime());
                 if (!do_scan) return;
@@ -445,7 +472,7 @@ persistent_ws_kernel(const WsParams wp) {
 #pragma unroll
                         for (int k = 0; k < D; k++) {
                             z[k] = dx[k];
-                            xn[i * D + k] = __ldcg(cur + (base + r) * D + k) + dx[k];
+                            xn[i * D + k] = xold[i * D + k] + dx[k];
                         }
                     }
                 }
@@ -484,34 +511,68 @@ persistent_ws_kernel(const WsParams wp) {
                 // per-item element stays live in registers
                 Elem<D> agg;
                 bool has = false;
+                // one item's element is staged to shared memory (for the apply)
+                // and folded into the thread's running aggregate as soon as it
+                // is built; explicit steps are built WS_PAIR at a time, stage by
+                // stage, for instruction-level parallelism
+                auto take = [&](int q, long long k, const Elem<D>& e, const double* h, bool sing) {
+                    rn = nan_drop_max(rn, row_max_abs<D>(h));
+                    if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
+                    if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
+                    if (do_scan) {
+                        double* dst = &sm.els[b][tid * EST + q * E];
 #pragma unroll
-                for (int q = 0; q < ITEMS; q++) {
-                    const int r = tid * ITEMS + q;
-                    const long long k = base + r;
-                    if (k < N) {
-                        double prev[D], xk[D], h[D];
+                        for (int kk = 0; kk < D * D; kk++) dst[kk] = e.F[kk];
 #pragma unroll
-                        for (int j = 0; j < D; j++) {
-                            prev[j] = row(b, r - 1, j);
-                            xk[j] = row(b, r, j);
+                        for (int kk = 0; kk < D; kk++) dst[D * D + kk] = e.c[kk];
+                        if (has)
+                            compose<D>(agg, e, agg);
+                        else {
+                            agg = e;
+                            has = true;
                         }
-                        Elem<D> e;
-                        bool sing = build_step<P, KIND, S>(prob, p.sc, prev, xk, k == 0, e, h);
-                        rn = nan_drop_max(rn, row_max_abs<D>(h));
-                        if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
-                        if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
-                        if (do_scan) {
-                            double* dst = &sm.els[b][tid * EST + q * E];
+                    }
+                };
+                constexpr int NP = (KIND == 0 && ITEMS % WS_PAIR == 0) ? WS_PAIR : 1;
 #pragma unroll
-                            for (int kk = 0; kk < D * D; kk++) dst[kk] = e.F[kk];
+                for (int q0 = 0; q0 < ITEMS; q0 += NP) {
+                    const long long k0 = base + tid * ITEMS + q0;
+                    if constexpr (NP > 1) {
+                        if (k0 + NP <= N) {
+                            double prev[NP][D], xk[NP][D], h[NP][D];
+                            bool first[NP];
+                            Elem<D> e[NP];
 #pragma unroll
-                            for (int kk = 0; kk < D; kk++) dst[D * D + kk] = e.c[kk];
-                            if (has)
-                                compose<D>(agg, e, agg);
-                            else {
-                                agg = e;
-                                has = true;
+                            for (int n = 0; n < NP; n++) {
+                                const int r = tid * ITEMS + q0 + n;
+#pragma unroll
+                                for (int j = 0; j < D; j++) {
+                                    prev[n][j] = row(b, r - 1, j);
+                                    xk[n][j] = row(b, r, j);
+                                }
+                                first[n] = (k0 + n == 0);
                             }
+                            build_explicit_multi<P, S, NP>(prob, p.sc, prev, xk, first, e, h);
+#pragma unroll
+                            for (int n = 0; n < NP; n++) take(q0 + n, k0 + n, e[n], h[n], false);
+                            continue;
+                        }
+                    }
+#pragma unroll
+                    for (int n = 0; n < NP; n++) {
+                        const int q = q0 + n;
+                        const int r = tid * ITEMS + q;
+                        const long long k = base + r;
+                        if (k < N) {
+                            double prev[D], xk[D], h[D];
+#pragma unroll
+                            for (int j = 0; j < D; j++) {
+                                prev[j] = row(b, r - 1, j);
+                                xk[j] = row(b, r, j);
+                            }
+                            Elem<D> e;
+                            const bool sing = build_step<P, KIND, S>(prob, p.sc, prev, xk, k == 0, e, h);
+                            take(q, k, e, h, sing);
                         }
                     }
                 }
