@@ -11,6 +11,8 @@
 // buffers; caller buffers that are already page-locked skip the staging copy
 // (DMA to / from them directly).  Calls are serialised by a mutex (the caches
 // are shared).
+#include <pthread.h>
+
 #include <atomic>
 #include <emmintrin.h>
 #include <chrono>
@@ -101,11 +103,13 @@ inline void nt_copy(char* dst, const char* src, size_t n) {
 class CopyPool {
   public:
     static CopyPool& get() {
-        static CopyPool pool;
-        return pool;
+        // intentionally never destroyed: its threads simply end with the process
+        static CopyPool* pool = new CopyPool();
+        return *pool;
     }
     void copy(void* dst, const void* src, size_t n) {
-        const int T = (int)workers_.size();
+        // a forked child has no worker threads (fork copies only the caller)
+        const int T = forked_.load(std::memory_order_relaxed) ? 0 : (int)workers_.size();
         if (T == 0 || n < (size_t(1) << 19)) {
             nt_copy(static_cast<char*>(dst), static_cast<const char*>(src), n);
             return;
@@ -129,19 +133,11 @@ class CopyPool {
 
   private:
     CopyPool() {
+        pthread_atfork(nullptr, nullptr, [] { get().forked_.store(true); });
         const char* e = std::getenv("ODX_HOST_THREADS");
         int t = e ? std::atoi(e) : 4;
         if (t > 1)
             for (int i = 0; i < t - 1; i++) workers_.emplace_back([this, i] { run(i); });
-    }
-    ~CopyPool() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-            gen_++;
-        }
-        cv_.notify_all();
-        for (auto& w : workers_) w.join();
     }
     void run(int i) {
         unsigned long long seen = 0;
@@ -153,7 +149,6 @@ class CopyPool {
                 std::unique_lock<std::mutex> lk(mu_);
                 cv_.wait(lk, [&] { return gen_ != seen; });
                 seen = gen_;
-                if (stop_) return;
                 d = dst_, s = src_, n = n_, chunk = chunk_;
             }
             const size_t lo = (size_t)i * chunk;
@@ -165,11 +160,11 @@ class CopyPool {
     std::mutex mu_;
     std::condition_variable cv_;
     unsigned long long gen_ = 0;
-    bool stop_ = false;
     char* dst_ = nullptr;
     const char* src_ = nullptr;
     size_t n_ = 0, chunk_ = 0;
     std::atomic<int> pending_{0};
+    std::atomic<bool> forked_{false};
 };
 
 // page-locked (cudaHostAlloc / registered) host memory can be a DMA endpoint
