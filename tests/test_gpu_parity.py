@@ -457,3 +457,76 @@ def test_host_buffer_path_matches_device_path(pkg):
             it = int(host.iterations_run[0])
             assert np.isnan(host.residual_history[0, it + 1:]).all()
     assert np.array_equal(pinned.numpy(), guess)  # the guess is never written
+
+
+# ------------------------------------------ path boundaries and edge cases ----
+
+# N values straddling every kernel-selection boundary for d = 2: the resident
+# CTA (N <= 2048), the grid-resident wave (2-item tiles up to 37888 steps,
+# 4-item tiles up to a full co-resident wave) and the streaming kernel beyond;
+# tiny and ragged sizes included.
+_BOUNDARY_N = [1, 2, 3, 255, 257, 2047, 2048, 2049, 4097, 37888, 37889, 65537, 200_003,
+               240_001, 300_007]
+
+
+@pytest.mark.parametrize("n", _BOUNDARY_N)
+@pytest.mark.parametrize("sname", ["rk4", "backward_euler"])
+def test_path_boundaries_vs_oracle(pkg, oracle, n, sname):
+    """Every launch path, at and around its size limits, against the oracle:
+    iterates, residual histories and statuses after 3 fixed iterations.
+    (Backward Euler runs VdP mu=10, whose iterates overflow to inf/NaN rows:
+    mu=1 grows them to ~1e64 over 300k steps, where the recursion amplifies
+    the rounding difference of any two association orders past 1e-9.)"""
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    dt = 1e-3
+    mu = 1.0 if sname == "rk4" else 10.0
+    prob = pkg.van_der_pol(mu=mu, x0=(2.0, 0.0), tf=n * dt)
+    st = pkg.get_stepper(sname, prob)
+    x0 = np.array([2.0, 0.0])
+    conf = pkg.NewtonConfig(max_iters=3, abort_on_nonfinite=False)
+    r = solve_batch(prob, st, dt, x0[None], None, conf)
+    ref = oracle.solve(1, (mu,), oracle.stepper_by_name(sname), x0, np.tile(x0, (n, 1)), dt, 3,
+                       abort_nonfinite=False)
+    assert int(r.iterations_run[0]) == ref["iters"] and int(r.status[0]) == ref["status"]
+    scaled_close(r.residual_history[0], ref["hist"], 1e-7, f"N={n} hist")
+    scaled_close(r.states[0], ref["X"], TOL, f"N={n} states")
+
+
+@pytest.mark.parametrize("n", [1000, 50_000, 300_000])
+def test_singular_block_every_path(pkg, oracle, n):
+    """A singular backward-Euler block (dy/dt = y^2 at y = 1/(2 dt)) placed in
+    the guess: SINGULAR with the smallest singular step, through the resident,
+    grid-resident and streaming kernels, as the oracle reports."""
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    dt = 0.1
+    prob = pkg.problems.square(x0=(0.5,), tf=n * dt)
+    st = pkg.get_stepper("backward_euler", prob)
+    guess = np.full((n, 1), 0.5)
+    bad = [n // 3, n // 2, n - 1]
+    guess[bad, 0] = 1.0 / (2.0 * dt)
+    conf = pkg.NewtonConfig(max_iters=2, abort_on_nonfinite=True)
+    r = solve_batch(prob, st, dt, np.array([[0.5]]), guess[None], conf)
+    ref = oracle.solve(9, (), oracle.stepper_by_name("backward_euler"), np.array([0.5]), guess,
+                       dt, 2, abort_nonfinite=True)
+    assert int(r.status[0]) == ref["status"] and int(r.status_index[0]) == ref["status_index"] == n // 3
+
+
+@pytest.mark.parametrize("n", [1000, 50_000, 300_000])
+def test_nonfinite_guess_every_path(pkg, oracle, n):
+    """NaN / inf rows in the guess: NONFINITE(0) when aborting (the residual
+    is inf), and identical non-finite row masks and finite values when not."""
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    dt = 1e-3
+    prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
+    st = pkg.get_stepper("rk4", prob)
+    x0 = np.array([2.0, 0.0])
+    guess = np.tile(x0, (n, 1))
+    guess[n // 2, 1] = np.nan
+    guess[n // 4, 0] = np.inf
+    for abort, iters in ((True, 3), (False, 2)):
+        conf = pkg.NewtonConfig(max_iters=iters, abort_on_nonfinite=abort)
+        r = solve_batch(prob, st, dt, x0[None], guess[None], conf)
+        ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), x0, guess, dt, iters,
+                           abort_nonfinite=abort)
+        assert int(r.status[0]) == ref["status"] and int(r.status_index[0]) == ref["status_index"]
+        scaled_close(r.states[0], ref["X"], TOL, f"N={n} abort={abort}")
