@@ -24,6 +24,10 @@ template <class P, int KIND, int S>
 int build_op(const ProbParams& pp, const StepCoefs& sc, const double* x0, const double* X,
              long long N, double* Fe, double* ce, double* h, long long* first_bad,
              cudaStream_t st, long long offset);
+template <class P, int KIND, int S>
+int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
+                      const double* X_local, long long n, long long offset, double* record,
+                      void* ws, size_t ws_bytes, cudaStream_t st);
 int scan_op(const double* F, const double* c, long long N, int d, double* Fp, double* cp,
             void* ws, size_t ws_bytes, cudaStream_t st);
 size_t scan_op_ws(long long N, int d);
@@ -92,6 +96,24 @@ struct BuildFn {
     int operator()() {
         return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
             return build_op<Q, K, SS>(*pp, *sc, x0, X, N, Fe, ce, h, fb, st, offset);
+        });
+    }
+};
+
+struct ShardLocalFn {
+    const odx_stepper* S;
+    const ProbParams* pp;
+    const StepCoefs* sc;
+    const double *halo, *X;
+    long long n, offset;
+    double* record;
+    void* ws;
+    size_t ws_bytes;
+    cudaStream_t st;
+    template <class PP>
+    int operator()() {
+        return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
+            return shard_tiled_local<Q, K, SS>(*pp, *sc, halo, X, n, offset, record, ws, ws_bytes, st);
         });
     }
 };
@@ -228,6 +250,18 @@ int build_common_offset(const odx_problem* P, const odx_stepper* S, int kind, co
                               reinterpret_cast<long long*>(first_bad), st);
     BuildFn fn{S, &pp, &sc, x0, X, N, Fe, ce, h, reinterpret_cast<long long*>(first_bad), st};
     fn.offset = offset;
+    return with_small_problem(P->problem_id, P->dim, fn);
+}
+
+// one rank's local pass of the time-sharded iteration (shard.cu validates)
+int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
+                         const double* halo, const double* X_local, long long n, long long offset,
+                         double* record, void* ws, size_t ws_bytes, cudaStream_t st) {
+    ProbParams pp;
+    StepCoefs sc;
+    if (!fill_params(P, pp)) return fail(ODX_EINVAL, "bad problem parameters");
+    if (!fill_coefs(S, dt, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
+    ShardLocalFn fn{S, &pp, &sc, halo, X_local, n, offset, record, ws, ws_bytes, st};
     return with_small_problem(P->problem_id, P->dim, fn);
 }
 }  // namespace odx

@@ -354,8 +354,8 @@ resident_solve_kernel(const SolveParams p) {
 // ---------------------------------------------------------------------------
 struct GridResParams {
     SolveParams sp;
-    double* aggs;      // G x (D*D + D)
-    void* halos;       // G x D chunks {value, tag}
+    double* aggs;      // 2 x G x (D*D + D): tile aggregates by iteration parity
+    void* halos;       // G rows {tag, v[4]} (HaloRow)
 };
 
 template <int D>
@@ -409,8 +409,15 @@ grid_resident_kernel(const GridResParams gp) {
     __shared__ int s_whas[NW];
 
     const SolveParams& p = gp.sp;
-    struct HChunk { double v; unsigned long long tag; };
-    HChunk* halos = reinterpret_cast<HChunk*>(gp.halos);
+    // CTA g's last row for CTA g+1: values first, then the tag with release
+    // semantics; the reader acquires the tag before reading the values (a
+    // 16-byte {value, tag} access is not single-copy atomic: a torn read can
+    // pair the new tag with the previous iterate's value)
+    struct alignas(64) HaloRow {
+        unsigned long long tag;
+        double v[4];
+    };
+    HaloRow* halos = reinterpret_cast<HaloRow*>(gp.halos);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const long long g = blockIdx.x;
     const unsigned G = gridDim.x;
@@ -442,20 +449,21 @@ grid_resident_kernel(const GridResParams gp) {
         for (int ii = 0; ii < ITEMS; ii++) {
             const int i = (ii + 1) % ITEMS;
             if (i == 0 && tid == 0 && it > 0 && g > 0) {
+                const HaloRow* src = halos + (g - 1);
+                const unsigned long long want = (unsigned long long)it;
+                unsigned long long tag;
+                int spins = 0;
+                while (true) {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];"
+                                 : "=l"(tag) : "l"(&src->tag) : "memory");
+                    if (tag == want) break;
+                    if (++spins > 8) __nanosleep(20);
+                }
 #pragma unroll
                 for (int k = 0; k < D; k++) {
-                    const HChunk* src = halos + (g - 1) * D + k;
-                    const unsigned long long want = (unsigned long long)it;
-                    unsigned long long tag;
-                    long long v;
-                    int spins = 0;
-                    while (true) {
-                        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
-                                     : "=l"(v), "=l"(tag) : "l"(src) : "memory");
-                        if (tag == want) break;
-                        if (++spins > 8) __nanosleep(20);
-                    }
-                    sm.xs[L::idx(k)] = __longlong_as_double(v);
+                    double v;
+                    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(&src->v[k]) : "memory");
+                    sm.xs[L::idx(k)] = v;
                 }
             }
             E::build_item(prob, p.sc, sm, base, N, i, el[i], rn, scn, bad);
@@ -496,7 +504,10 @@ grid_resident_kernel(const GridResParams gp) {
                 Elem<D> A;
                 bool A_has = false;
                 E::tile_aggregate(sm, A, A_has);
-                double* dst = gp.aggs + g * EA;
+                // double-buffered by iteration parity: a CTA that is already
+                // publishing iteration it+1 must not overwrite aggregates a
+                // slower CTA is still folding for iteration it
+                double* dst = gp.aggs + ((long long)(it & 1) * G + g) * EA;
 #pragma unroll
                 for (int k = 0; k < D * D; k++) dst[k] = A.F[k];
 #pragma unroll
@@ -519,7 +530,7 @@ grid_resident_kernel(const GridResParams gp) {
             const long long lo = tid * per, hi = (lo + per < g) ? lo + per : g;
             for (long long q = lo; q < hi; q++) {
                 Elem<D> a;
-                const double* src = gp.aggs + q * EA;
+                const double* src = gp.aggs + ((long long)(it & 1) * G + q) * EA;
 #pragma unroll
                 for (int k = 0; k < D * D; k++) a.F[k] = __ldcg(src + k);
 #pragma unroll
@@ -581,14 +592,15 @@ grid_resident_kernel(const GridResParams gp) {
         // the thread that owns the last row hands it to CTA g+1 (tag = next
         // iteration) as soon as it has written it
         if (g + 1 < G && tid == (int)((rows - 1) / ITEMS)) {
+            HaloRow* dst = halos + g;
 #pragma unroll
             for (int k = 0; k < D; k++) {
                 const double v = sm.xs[L::idx((int)rows * D + k)];
-                HChunk* dst = halos + g * D + k;
-                asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(dst),
-                             "l"(__double_as_longlong(v)), "l"((unsigned long long)(it + 1))
-                             : "memory");
+                asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(&dst->v[k]), "d"(v) : "memory");
             }
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&dst->tag),
+                         "l"((unsigned long long)(it + 1))
+                         : "memory");
         }
         // max|dx|: warp maxima now; the block max and its atomic ride on the
         // next iteration's reduction (before that iteration's barrier)

@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "dispatch.cuh"
 #include "solve_small.cuh"
+#include "solve_tiled.cuh"
 #include "solve_ws.cuh"
 
 namespace odx {
@@ -103,9 +104,9 @@ int launch_grid_resident(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t
     auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
     const size_t o_red = at(4 * ((size_t)p.max_iters + 1) * 8);
     const size_t o_bar = at(8);
-    const size_t o_halo = at((size_t)G * D * 16);
+    const size_t o_halo = at((size_t)G * 64);  // HaloRow
     const size_t zero_end = off;
-    const size_t o_aggs = at((size_t)G * (D * D + D) * 8);
+    const size_t o_aggs = at(2 * (size_t)G * (D * D + D) * 8);  // by iteration parity
     const size_t total = off + 256;
     if (query) {
         *need = total;
@@ -126,6 +127,92 @@ int launch_grid_resident(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t
     ODX_CUDA(cudaGetLastError());
     count_launch(2);
     return ODX_OK;
+}
+
+
+// Tiled two-pass solve (solve_tiled.cuh) of one trajectory: 3 kernels per
+// Newton iteration, every iteration enqueued up front.
+template <int D>
+struct TiledLayout {
+    size_t total = 0, el, cagg, cpre, red, stop;
+    long long ntiles;
+    TiledLayout(long long N, long long T, int max_iters, int nchunks) {
+        ntiles = (N + T - 1) / T;
+        constexpr int E = D * D + D;
+        size_t off = 0;
+        auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
+        red = at(4 * ((size_t)max_iters + 1) * 8);  // first: init_ws sets its bad slots
+        stop = at(8);
+        el = at((size_t)N * E * 8);
+        cagg = at((size_t)nchunks * E * 8);
+        cpre = at(((size_t)nchunks + 1) * E * 8);
+        total = off + 256;
+    }
+};
+
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+int launch_tiled(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
+                 size_t* need) {
+    constexpr int D = P::D;
+    constexpr long long T = (long long)THREADS * ITEMS;
+    auto k1 = tiled_build_kernel<P, KIND, S, THREADS, ITEMS>;
+    auto k3 = tiled_apply_kernel<D, THREADS, ITEMS>;
+    auto k2 = tiled_scan_kernel<D>;
+    const size_t smem3 = sizeof(TiledApplySmem<D, THREADS, ITEMS>);
+    int o1 = 1, o3 = 1;
+    if (!query) {
+        if (int rc = kernel_occupancy((const void*)k1, THREADS, 0, &o1)) return rc;
+        if (int rc = kernel_occupancy((const void*)k3, THREADS, smem3, &o3)) return rc;
+    }
+    const long long ntiles = (p.N + T - 1) / T;
+    // one chunking for K1 and K3 (a chunk per resident CTA of the slower one)
+    long long nch = (long long)(o1 < o3 ? o1 : o3) * num_sms();
+    if (nch > 4LL * num_sms()) nch = 4LL * num_sms();  // the workspace query's bound
+    if (nch < 1) nch = 1;
+    if (nch > ntiles) nch = ntiles;
+    const TiledLayout<D> lay(p.N, T, p.max_iters, query ? 4 * num_sms() : (int)nch);
+    if (query) {
+        *need = lay.total;
+        return ODX_OK;
+    }
+    if (ws == nullptr || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "workspace too small");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    TiledParams tp;
+    tp.sp = p;
+    tp.sp.red = reinterpret_cast<unsigned long long*>(base + lay.red);
+    tp.el = reinterpret_cast<double*>(base + lay.el);
+    tp.cagg = reinterpret_cast<double*>(base + lay.cagg);
+    tp.cpre = reinterpret_cast<double*>(base + lay.cpre);
+    tp.stop = reinterpret_cast<int*>(base + lay.stop);
+    tp.halo = p.x0;
+    tp.carry = nullptr;
+    tp.offset = 0;
+    tp.ntiles = lay.ntiles;
+    tp.nchunks = (int)nch;
+    tp.decide_here = 1;
+    tp.kind = KIND;
+    init_ws(base, lay.stop + 8, p.max_iters + 1, st);
+    int launches = 1;
+    for (int it = 0; it <= p.max_iters; it++) {
+        k1<<<(unsigned)nch, THREADS, 0, st>>>(tp, it);
+        k2<<<1, 32, 0, st>>>(tp, it);
+        launches += 2;
+        if (it < p.max_iters) {
+            k3<<<(unsigned)nch, THREADS, smem3, st>>>(tp, it);
+            launches += 1;
+        }
+    }
+    ODX_CUDA(cudaGetLastError());
+    count_launch(launches);
+    return ODX_OK;
+}
+
+inline bool use_tiled() {
+    static const bool on = [] {
+        const char* v = std::getenv("ODX_TILED");
+        return v && std::strcmp(v, "1") == 0;
+    }();
+    return on;
 }
 
 inline bool use_grid_resident() {
@@ -173,6 +260,8 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
             rc = launch_grid_resident<P, KIND, S, 128, GI>(p, ws, ws_bytes, st, query, need);
         if (rc != ODX_EUNSUPPORTED) return rc;
     }
+    if (!resident && p.B == 1 && use_tiled())  // (static smem: T*E*8 <= 48 KB)
+        return launch_tiled<P, KIND, S, 128, (D <= 2 ? 4 : 2)>(p, ws, ws_bytes, st, query, need);
     if (query) {
         *need = 0;
         if (!resident) {

@@ -530,3 +530,27 @@ def test_nonfinite_guess_every_path(pkg, oracle, n):
                            abort_nonfinite=abort)
         assert int(r.status[0]) == ref["status"] and int(r.status_index[0]) == ref["status_index"]
         scaled_close(r.states[0], ref["X"], TOL, f"N={n} abort={abort}")
+
+
+def test_grid_resident_stress_cold_memory(pkg, oracle):
+    """Regression: the grid-resident kernel once kept its tile aggregates in a
+    single buffer, so a CTA already publishing iteration it+1 could overwrite
+    aggregates a slower CTA was still folding for iteration it.  Cold memory
+    (a 3 GB sweep between solves) made CTAs uneven enough to show it.  Every
+    history entry and iterate must match the oracle on every repetition."""
+    import torch
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    n, dt = 200_003, 1e-3
+    prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
+    st = pkg.get_stepper("rk4", prob)
+    x0 = np.array([2.0, 0.0])
+    ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), x0, np.tile(x0, (n, 1)), dt, 3,
+                       abort_nonfinite=False)
+    sweep = torch.empty(3 << 27, dtype=torch.float64, device="cuda")  # 3 GiB
+    conf = pkg.NewtonConfig(max_iters=3, abort_on_nonfinite=False)
+    for _ in range(4):
+        sweep.fill_(0.0)
+        r = solve_batch(prob, st, dt, x0[None], None, conf)
+        scaled_close(r.residual_history[0], ref["hist"], 1e-7, "hist")
+        scaled_close(r.states[0], ref["X"], TOL, "states")
+    del sweep
