@@ -66,6 +66,12 @@ extern "C" {
 #define ODX_PROB_LINEAR      10  /* dx/dt = A x; params: A row-major (dim<=8)      */
 #define ODX_NUM_PROBLEMS     11
 
+/* initial-guess policies (newton_pint.initial_guess, newton_pint.py:174-207) */
+#define ODX_GUESS_ONES         0
+#define ODX_GUESS_ZEROS        1
+#define ODX_GUESS_REPLICATE_X0 2
+#define ODX_GUESS_COARSE_EULER 3
+
 #define ODX_MAX_PARAMS 64
 
 typedef struct odx_problem {
@@ -140,6 +146,14 @@ int odx_solve_host(const odx_problem* P, const odx_stepper* S,
                    int64_t B, int64_t N, double dt, const odx_newton_cfg* C,
                    double* hist, double* scaled_hist,
                    int32_t* iters, int32_t* status, int64_t* status_index, void* stream);
+
+/* The starting iterate built on the device (newton_pint.initial_guess
+ * :174-207): X (B x N x d, device) from x0 (B x d, device) by an
+ * ODX_GUESS_* policy; dt = (tf - t0) / N as the reference computes it
+ * (coarse_euler: stride max(1, N/100), v += (stride*dt) f(v), each coarse
+ * value held over the next stride rows).                                    */
+int odx_initial_guess(const odx_problem* P, int32_t policy, const double* x0, double* X,
+                      int64_t B, int64_t N, double dt, void* stream);
 
 /* ---- piecewise ops mirroring the reference's compiled loops ---------------- */
 /* _kernels.build_explicit  _kernels.py:299-342 (+ _rk_increment_with_jac :261-296) */

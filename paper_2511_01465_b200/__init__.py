@@ -11,6 +11,7 @@ from .affine_scan import (AffineElement, combine, extract_states, identity, init
                           scan_parallel, scan_sequential)
 from .newton_pint import (GUESS_POLICIES, BatchSolveReport, NewtonConfig, NonFiniteError,
                           SingularDiagonalBlockError, SolveReport, Trajectory, initial_guess,
+                          initial_guess_device,
                           n_steps_for, solve, solve_batch)
 from .problems import (EXTRA_PROBLEM_NAMES, PROBLEM_NAMES, OdeProblem, allen_cahn, cart_pole,
                        dahlquist, get_problem, logistic, lorenz63, robertson, van_der_pol)
@@ -24,7 +25,7 @@ __all__ = [
     "AffineElement", "combine", "identity", "init_elements", "scan_parallel",
     "scan_sequential", "extract_states", "GUESS_POLICIES", "NewtonConfig", "NonFiniteError",
     "SingularDiagonalBlockError", "SolveReport", "BatchSolveReport", "Trajectory",
-    "initial_guess", "n_steps_for", "solve", "solve_batch", "PROBLEM_NAMES",
+    "initial_guess", "initial_guess_device", "n_steps_for", "solve", "solve_batch", "PROBLEM_NAMES",
     "EXTRA_PROBLEM_NAMES", "OdeProblem", "cart_pole", "dahlquist", "get_problem", "logistic",
     "robertson", "van_der_pol", "lorenz63", "allen_cahn", "EULER_TABLEAU", "RK4_TABLEAU",
     "STEPPER_NAMES", "ButcherTableau", "StepperIncrement", "explicit_euler", "explicit_rk",

@@ -19,9 +19,12 @@ struct AllenCahnRows {
         : cdiff(q.p[0] / (q.p[1] * q.p[1])) {
         (void)dim;
     }
+    // non-contracted, as numpy evaluates it (problems.allen_cahn f_into)
     __device__ __forceinline__ double f(const double* x, int i) const {
         const double um = x[(i + n - 1) % n], ui = x[i], up = x[(i + 1) % n];
-        return cdiff * ((um - 2.0 * ui) + up) + (ui - ui * ui * ui);
+        const double lap = __dadd_rn(__dsub_rn(um, __dmul_rn(2.0, ui)), up);
+        const double cub = __dsub_rn(ui, __dmul_rn(__dmul_rn(ui, ui), ui));
+        return __dadd_rn(__dmul_rn(cdiff, lap), cub);
     }
     // Row i's entries that can be non-zero, as (column, value) pairs with the
     // same values jac(x, i, j) returns; every other entry of row i is 0.0.

@@ -30,7 +30,7 @@ from .steppers import StepperIncrement
 __all__ = [
     "Trajectory", "NewtonConfig", "SolveReport", "BatchSolveReport",
     "SingularDiagonalBlockError", "NonFiniteError", "n_steps_for", "initial_guess", "solve",
-    "solve_batch", "solve_device", "GUESS_POLICIES",
+    "solve_batch", "solve_device", "GUESS_POLICIES", "initial_guess_device",
 ]
 
 GUESS_POLICIES = ("ones", "zeros", "replicate_x0", "coarse_euler")
@@ -178,6 +178,31 @@ def initial_guess(policy: str, problem: OdeProblem, n_steps: int) -> Trajectory:
         raise ValueError(f"unknown initial-guess policy {policy!r}; "
                          f"available: {', '.join(GUESS_POLICIES)}")
     return Trajectory(problem.x0.copy(), states, dt, n_steps)
+
+
+_GUESS_IDS = {"ones": 0, "zeros": 1, "replicate_x0": 2, "coarse_euler": 3}
+
+
+def initial_guess_device(policy: str, problem: OdeProblem, n_steps: int, x0s=None, device=None):
+    """initial_guess (newton_pint.py:174-207) built on the GPU: a (B, N, d)
+    CUDA tensor, B = len(x0s) (default: problem.x0).  No host construction,
+    no host-to-device copy of the O(N d) states."""
+    import torch
+    if policy not in _GUESS_IDS:
+        raise ValueError(f"unknown initial-guess policy {policy!r}; "
+                         f"available: {', '.join(GUESS_POLICIES)}")
+    if problem.device is None:
+        raise ValueError(f"problem {problem.name!r} has no CUDA functor")
+    dev = _device(device)
+    x0 = problem.x0[None] if x0s is None else x0s
+    x0t = (x0.detach().to(dev, torch.float64).contiguous() if _is_torch(x0)
+           else torch.as_tensor(np.ascontiguousarray(x0, dtype=np.float64), device=dev))
+    B, d = x0t.shape
+    X = torch.empty((B, n_steps, d), dtype=torch.float64, device=dev)
+    dt = (problem.tf - problem.t0) / n_steps  # as the reference computes it
+    N.check(N.lib().odx_initial_guess(problem.native(), _GUESS_IDS[policy], N.ptr(x0t), N.ptr(X),
+                                      B, n_steps, float(dt), N.stream_handle(dev)))
+    return X
 
 
 def _resolve_guess(guess, problem: OdeProblem, n: int, dt: float) -> Trajectory:
@@ -379,7 +404,11 @@ def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones
     dev = _device(device)
 
     t_begin = time.perf_counter()
-    start = _resolve_guess(guess, problem, n, dt)
+    if isinstance(guess, str):  # a policy: build the starting iterate on the GPU
+        start = Trajectory(problem.x0.copy(),
+                           initial_guess_device(guess, problem, n, device=dev)[0], dt, n)
+    else:
+        start = _resolve_guess(guess, problem, n, dt)
     if output != "torch" and not _is_torch(start.states):
         states, hist, shist, iters, status, sidx = _solve_host(
             P, S, np.asarray(problem.x0, dtype=np.float64).reshape(1, -1),
@@ -461,9 +490,8 @@ def solve_batch(problem: OdeProblem, stepper: StepperIncrement, dt: float, x0s, 
         raise ValueError(f"x0s has dim {d}, expected {problem.dim}")
     if guess is None:
         X = x0t[:, None, :].expand(B, n, d).contiguous()
-    elif isinstance(guess, str):
-        g = initial_guess(guess, problem, n).states
-        X = _to_device(g, dev, ("X", dev))[None].expand(B, n, d).contiguous()
+    elif isinstance(guess, str):  # the policy applied to each trajectory's x0, on the GPU
+        X = initial_guess_device(guess, problem, n, x0s=x0t, device=dev)
     elif _is_torch(guess):
         X = guess.detach().to(dev, torch.float64).clone().contiguous()
     else:

@@ -554,3 +554,40 @@ def test_grid_resident_stress_cold_memory(pkg, oracle):
         scaled_close(r.residual_history[0], ref["hist"], 1e-7, "hist")
         scaled_close(r.states[0], ref["X"], TOL, "states")
     del sweep
+
+
+@pytest.mark.parametrize("name", ["vdp", "lorenz", "allen_cahn", "logistic"])
+def test_initial_guess_on_device(pkg, name):
+    """initial_guess policies built on the GPU against the
+    host implementation of newton_pint.initial_guess (:174-207): ones, zeros
+    and replicate_x0 exactly; coarse_euler to f's rounding (1e-12)."""
+    from paper_2511_01465_b200.newton_pint import initial_guess, initial_guess_device
+    prob = {"vdp": lambda: pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=12.3),
+            "lorenz": lambda: pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=2.0),
+            "allen_cahn": lambda: pkg.allen_cahn(tf=1.0),
+            "logistic": lambda: pkg.problems.logistic(tf=5.0)}[name]()
+    for n in (7, 100, 4097):
+        for policy in ("ones", "zeros", "replicate_x0", "coarse_euler"):
+            host = initial_guess(policy, prob, n).states
+            devg = initial_guess_device(policy, prob, n)[0].cpu().numpy()
+            if policy == "coarse_euler":
+                scaled_close(devg, host, 1e-12, f"{name} {policy} N={n}")
+            else:
+                assert np.array_equal(devg, host), (name, policy, n)
+
+
+def test_solve_with_device_built_guess(pkg, oracle):
+    """solve(guess="coarse_euler") builds the guess on the GPU; the iterates
+    match the oracle run from the host-built guess."""
+    from paper_2511_01465_b200.newton_pint import initial_guess
+    n, dt = 20_000, 1e-3
+    prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
+    st = pkg.get_stepper("rk4", prob)
+    rep = pkg.solve(prob, st, dt, guess="coarse_euler",
+                    config=pkg.NewtonConfig(max_iters=3, residual_tol=0.0))
+    g = initial_guess("coarse_euler", prob, n).states
+    ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), np.array([2.0, 0.0]), g, dt, 3,
+                       abort_nonfinite=True)
+    assert rep.iterations_run == ref["iters"]
+    scaled_close(np.asarray(rep.residual_history), ref["hist"], 1e-7, "hist")
+    scaled_close(np.asarray(rep.trajectory.states), ref["X"], 1e-9, "states")
