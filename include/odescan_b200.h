@@ -155,6 +155,16 @@ int odx_solve_host(const odx_problem* P, const odx_stepper* S,
 int odx_initial_guess(const odx_problem* P, int32_t policy, const double* x0, double* X,
                       int64_t B, int64_t N, double dt, void* stream);
 
+/* Sequential marchers (baselines.solve_sequential_*), one GPU thread per
+ * trajectory, d <= 4.  Explicit stepper: _kernels.seq_explicit :345-360,
+ * X[b,k] = state after k+1 steps.  Implicit: _kernels.seq_implicit :467-526,
+ * a per-step Newton solve (tol, max_inner); status[b] (device int64) = -1,
+ * -(k+2) for a singular step-k system, or k when step k did not converge
+ * (X rows from that step on are left unwritten).                            */
+int odx_seq_march(const odx_problem* P, const odx_stepper* S, const double* x0, double* X,
+                  int64_t B, int64_t N, double dt, double tol, int32_t max_inner,
+                  int64_t* status, void* stream);
+
 /* ---- piecewise ops mirroring the reference's compiled loops ---------------- */
 /* _kernels.build_explicit  _kernels.py:299-342 (+ _rk_increment_with_jac :261-296) */
 int odx_build_explicit(const odx_problem* P, const odx_stepper* S,

@@ -7,6 +7,8 @@ importing this package does not load it — the first solve() does, and fails
 loudly if it is missing.
 """
 
+from .baselines import (InnerNewtonFailedError, solve_sequential_batch,
+                        solve_sequential_explicit, solve_sequential_implicit)
 from .affine_scan import (AffineElement, combine, extract_states, identity, init_elements,
                           scan_parallel, scan_sequential)
 from .newton_pint import (GUESS_POLICIES, BatchSolveReport, NewtonConfig, NonFiniteError,
@@ -22,6 +24,8 @@ from .steppers import (EULER_TABLEAU, RK4_TABLEAU, STEPPER_NAMES, ButcherTableau
 __version__ = "0.1.0"
 
 __all__ = [
+    "InnerNewtonFailedError", "solve_sequential_explicit", "solve_sequential_implicit",
+    "solve_sequential_batch",
     "AffineElement", "combine", "identity", "init_elements", "scan_parallel",
     "scan_sequential", "extract_states", "GUESS_POLICIES", "NewtonConfig", "NonFiniteError",
     "SingularDiagonalBlockError", "SolveReport", "BatchSolveReport", "Trajectory",

@@ -25,6 +25,10 @@ int build_op(const ProbParams& pp, const StepCoefs& sc, const double* x0, const 
              long long N, double* Fe, double* ce, double* h, long long* first_bad,
              cudaStream_t st, long long offset);
 template <class P, int KIND, int S>
+int seq_march(const ProbParams& pp, const StepCoefs& sc, double tol, int max_inner,
+              const double* x0, double* X, long long B, long long N, long long* status,
+              cudaStream_t st);
+template <class P, int KIND, int S>
 int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
                       const double* X_local, long long n, long long offset, double* record,
                       void* ws, size_t ws_bytes, cudaStream_t st);
@@ -96,6 +100,25 @@ struct BuildFn {
     int operator()() {
         return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
             return build_op<Q, K, SS>(*pp, *sc, x0, X, N, Fe, ce, h, fb, st, offset);
+        });
+    }
+};
+
+struct SeqFn {
+    const odx_stepper* S;
+    const ProbParams* pp;
+    const StepCoefs* sc;
+    double tol;
+    int max_inner;
+    const double* x0;
+    double* X;
+    long long B, N;
+    long long* status;
+    cudaStream_t st;
+    template <class PP>
+    int operator()() {
+        return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
+            return seq_march<Q, K, SS>(*pp, *sc, tol, max_inner, x0, X, B, N, status, st);
         });
     }
 };
@@ -267,6 +290,26 @@ int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
 }  // namespace odx
 
 extern "C" {
+
+int odx_seq_march(const odx_problem* P, const odx_stepper* S, const double* x0, double* X,
+                  int64_t B, int64_t N, double dt, double tol, int32_t max_inner,
+                  int64_t* status, void* stream) {
+    g_err.clear();
+    int rc = check_problem(P, S);
+    if (rc) return rc;
+    if (P->dim > 4) return fail(ODX_EUNSUPPORTED, "sequential marchers support d <= 4");
+    if (!x0 || !X || B < 1 || N < 0) return fail(ODX_EINVAL, "bad buffers or extents");
+    if (S->kind == ODX_STEP_IMPLICIT_WEIGHTED && (!status || max_inner < 1 || !(tol >= 0.0)))
+        return fail(ODX_EINVAL, "implicit march needs status, max_inner >= 1 and tol >= 0");
+    ProbParams pp;
+    StepCoefs sc;
+    if (!fill_params(P, pp)) return fail(ODX_EINVAL, "bad problem parameters");
+    if (!fill_coefs(S, dt, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
+    if (N == 0) return ODX_OK;
+    SeqFn fn{S, &pp, &sc, tol, max_inner, x0, X, B, N, reinterpret_cast<long long*>(status),
+             (cudaStream_t)stream};
+    return with_small_problem(P->problem_id, P->dim, fn);
+}
 
 int odx_build_explicit(const odx_problem* P, const odx_stepper* S, const double* x0,
                        const double* X, int64_t N, double dt, double* Fe, double* ce, double* h,

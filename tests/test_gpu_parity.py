@@ -591,3 +591,83 @@ def test_solve_with_device_built_guess(pkg, oracle):
     assert rep.iterations_run == ref["iters"]
     scaled_close(np.asarray(rep.residual_history), ref["hist"], 1e-7, "hist")
     scaled_close(np.asarray(rep.trajectory.states), ref["X"], 1e-9, "states")
+
+
+# ------------------------------------------ sequential marchers (§8f rank 3) --
+
+@pytest.mark.parametrize("case", [
+    ("vdp", "rk4", 20_000, 1e-3), ("lorenz", "rk4", 3_000, 1e-3), ("logistic", "euler", 5_000, 1e-2),
+    ("cartpole", "rk4", 10_000, 1e-3),
+])
+def test_sequential_explicit_vs_oracle(pkg, oracle, case):
+    """solve_sequential_explicit on the GPU against _kernels.seq_explicit
+    (:345-360) restated in the oracle."""
+    name, sname, n, dt = case
+    if name == "vdp":
+        prob, pid, params = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt), 1, (1.0,)
+    elif name == "lorenz":
+        prob, pid, params = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=n * dt), 6, (10.0, 28.0, 8.0 / 3.0)
+    elif name == "logistic":
+        prob = pkg.problems.logistic(tf=n * dt)
+        pid, params = 0, (1.0, 1.0)
+    else:
+        prob = pkg.problems.cart_pole()
+        prob = type(prob)(**{**prob.__dict__, "tf": n * dt})
+        pid, params = 2, (9.81, 0.5, 10.0, 1.0)
+    st = pkg.get_stepper(sname, prob)
+    tr = pkg.solve_sequential_explicit(prob, st, dt)
+    s = oracle.stepper_by_name(sname)
+    a = np.array([s.a[i] for i in range(s.stages * s.stages)]).reshape(s.stages, s.stages)
+    b = np.array([s.b[i] for i in range(s.stages)])
+    ref = oracle.seq_explicit(pid, params, a, b, prob.x0, dt, n)
+    scaled_close(tr.states, ref, 1e-9, f"{name} sequential")
+
+
+@pytest.mark.parametrize("case", [
+    ("dahlquist", 4, (-1000.0,), 0.1, 40), ("vdp10", 1, (10.0,), 1e-3, 20_000),
+    ("robertson", 5, (0.04, 3.0e7, 1.0e4), 1e-3, 5_000),
+])
+def test_sequential_implicit_vs_oracle(pkg, oracle, case):
+    """solve_sequential_implicit on the GPU against _kernels.seq_implicit
+    (:467-526): states and the per-step Newton outcome."""
+    name, pid, params, dt, n = case
+    if name == "dahlquist":
+        prob = pkg.dahlquist(lam=-1000.0)  # [0, 4]: 40 steps of 0.1
+    elif name == "vdp10":
+        prob = pkg.van_der_pol(mu=10.0, x0=(2.0, 0.0), tf=n * dt)
+    else:
+        prob = pkg.problems.robertson()
+        prob = type(prob)(**{**prob.__dict__, "tf": n * dt})
+    st = pkg.get_stepper("backward_euler", prob)
+    ref, code = oracle.seq_implicit(pid, prob.device[1], 0.0, 1.0, prob.x0, dt, n)
+    assert code == -1
+    tr = pkg.solve_sequential_implicit(prob, st, dt)
+    scaled_close(tr.states, ref, 1e-9, f"{name} sequential implicit")
+
+
+def test_sequential_errors_and_batch(pkg, oracle):
+    """InnerNewtonFailedError (singular and non-converged steps) as the
+    reference raises it; a batch of marches equals the single marches."""
+    from paper_2511_01465_b200.baselines import InnerNewtonFailedError
+    sq = pkg.problems.square(x0=(1.0,), tf=1.0)
+    with pytest.raises(InnerNewtonFailedError) as e:  # singular at y = 1/(2 dt) = 5
+        pkg.solve_sequential_implicit(sq, pkg.get_stepper("backward_euler", sq), 0.1,
+                                      n_steps=10, inner_max_iters=50)
+    _, code = oracle.seq_implicit(9, (), 0.0, 1.0, np.array([1.0]), 0.1, 10)
+    if code <= -2:
+        assert e.value.singular and e.value.step == -code - 2
+    else:
+        assert not e.value.singular and e.value.step == code
+    vdp = pkg.van_der_pol(mu=10.0, x0=(2.0, 0.0), tf=2.0)
+    with pytest.raises(InnerNewtonFailedError) as e2:
+        pkg.solve_sequential_implicit(vdp, pkg.get_stepper("backward_euler", vdp), 0.5,
+                                      n_steps=4, inner_max_iters=1, inner_newton_tol=0.0)
+    assert not e2.value.singular
+    prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=5.0)
+    st = pkg.get_stepper("rk4", prob)
+    x0s = np.array([[2.0, 0.0], [1.0, 1.0], [-0.5, 2.0]])
+    Xb, codes = pkg.solve_sequential_batch(prob, st, 1e-3, x0s)
+    assert (codes == -1).all()
+    for b in range(3):
+        ref = oracle.seq_explicit(1, (1.0,), oracle.RK4_A, oracle.RK4_B, x0s[b], 1e-3, 5000)
+        scaled_close(Xb[b], ref, 1e-9, f"batch {b}")

@@ -109,3 +109,27 @@ def test_baseline_configs_inputs():
     u0 = CONFIGS[4].x0s()[0]
     assert u0.shape == (64,) and abs(u0[16] - 0.1) < 0.05
     assert math.isclose(CONFIGS[1].params[2], 8.0 / 3.0)
+
+
+def test_sequential_baselines_validate_without_gpu():
+    """baselines.solve_sequential_* reject what the reference rejects
+    (baselines.py:64-125) before touching the device."""
+    import paper_2511_01465_b200 as pkg
+    p = pkg.van_der_pol()
+    rk4 = pkg.get_stepper("rk4", p)
+    be = pkg.get_stepper("backward_euler", p)
+    with pytest.raises(ValueError):
+        pkg.solve_sequential_explicit(p, be, 1e-3)
+    with pytest.raises(ValueError):
+        pkg.solve_sequential_implicit(p, rk4, 1e-3)
+    with pytest.raises(ValueError):
+        pkg.solve_sequential_implicit(p, be, 1e-3, inner_newton_tol=-1.0)
+    with pytest.raises(ValueError):
+        pkg.solve_sequential_implicit(p, be, 1e-3, inner_max_iters=0)
+    with pytest.raises(ValueError):
+        pkg.solve_sequential_explicit(p, rk4, 1e-3, n_steps=-1)
+    other = pkg.van_der_pol()
+    with pytest.raises(ValueError):
+        pkg.solve_sequential_explicit(other, rk4, 1e-3)
+    t = pkg.solve_sequential_explicit(p, rk4, 1e-3, n_steps=0)
+    assert t.states.shape == (0, 2)
