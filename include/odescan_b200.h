@@ -165,6 +165,15 @@ int odx_seq_march(const odx_problem* P, const odx_stepper* S, const double* x0, 
                   int64_t B, int64_t N, double dt, double tol, int32_t max_inner,
                   int64_t* status, void* stream);
 
+/* Parareal's sequential coarse sweep (baselines.solve_parareal :164-227) on
+ * the device: mode 0 nodes[0..m] = x0, G(x0), G(G(x0)), ... and g_prev = the
+ * G values; mode 1 nodes[k+1] = G(nodes[k]) + fine[k, sub-1] - g_prev[k]
+ * (g_prev updated).  G = one step of the explicit S_coarse of dt_coarse.
+ * The fine passes are odx_seq_march over the m start nodes.               */
+int odx_parareal_coarse(const odx_problem* P, const odx_stepper* S_coarse, const double* x0,
+                        double* nodes, double* g_prev, const double* fine, int32_t m,
+                        int64_t sub, double dt_coarse, int32_t mode, void* stream);
+
 /* ---- piecewise ops mirroring the reference's compiled loops ---------------- */
 /* _kernels.build_explicit  _kernels.py:299-342 (+ _rk_increment_with_jac :261-296) */
 int odx_build_explicit(const odx_problem* P, const odx_stepper* S,

@@ -7,8 +7,9 @@ importing this package does not load it — the first solve() does, and fails
 loudly if it is missing.
 """
 
-from .baselines import (InnerNewtonFailedError, solve_sequential_batch,
-                        solve_sequential_explicit, solve_sequential_implicit)
+from .baselines import (InnerNewtonFailedError, PararealConfig, PararealResult,
+                        solve_parareal, solve_sequential_batch, solve_sequential_explicit,
+                        solve_sequential_implicit)
 from .affine_scan import (AffineElement, combine, extract_states, identity, init_elements,
                           scan_parallel, scan_sequential)
 from .newton_pint import (GUESS_POLICIES, BatchSolveReport, NewtonConfig, NonFiniteError,
@@ -25,7 +26,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "InnerNewtonFailedError", "solve_sequential_explicit", "solve_sequential_implicit",
-    "solve_sequential_batch",
+    "solve_sequential_batch", "PararealConfig", "PararealResult", "solve_parareal",
     "AffineElement", "combine", "identity", "init_elements", "scan_parallel",
     "scan_sequential", "extract_states", "GUESS_POLICIES", "NewtonConfig", "NonFiniteError",
     "SingularDiagonalBlockError", "SolveReport", "BatchSolveReport", "Trajectory",

@@ -28,7 +28,7 @@ PROB_LINEAR = 10
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = (
     "odx_abi_version", "odx_last_error", "odx_supported", "odx_launch_count", "odx_solve_workspace_bytes",
-    "odx_solve", "odx_solve_host", "odx_initial_guess", "odx_seq_march", "odx_build_explicit", "odx_build_implicit",
+    "odx_solve", "odx_solve_host", "odx_initial_guess", "odx_seq_march", "odx_parareal_coarse", "odx_build_explicit", "odx_build_implicit",
     "odx_scan_affine_workspace_bytes", "odx_scan_affine", "odx_max_abs", "odx_add_inplace",
     "odx_shard_workspace_bytes", "odx_shard_local", "odx_shard_fixup",
 )
@@ -86,6 +86,8 @@ def lib():
     L.odx_initial_guess.argtypes = [P_, i32, vp, vp, i64, i64, dbl, vp]
     L.odx_seq_march.restype = C.c_int
     L.odx_seq_march.argtypes = [P_, S_, vp, vp, i64, i64, dbl, dbl, i32, vp, vp]
+    L.odx_parareal_coarse.restype = C.c_int
+    L.odx_parareal_coarse.argtypes = [P_, S_, vp, vp, vp, vp, i32, i64, dbl, i32, vp]
     L.odx_build_explicit.restype = C.c_int
     L.odx_build_explicit.argtypes = [P_, S_, vp, vp, i64, dbl, vp, vp, vp, vp]
     L.odx_build_implicit.restype = C.c_int

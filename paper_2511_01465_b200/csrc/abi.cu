@@ -29,6 +29,10 @@ int seq_march(const ProbParams& pp, const StepCoefs& sc, double tol, int max_inn
               const double* x0, double* X, long long B, long long N, long long* status,
               cudaStream_t st);
 template <class P, int KIND, int S>
+int parareal_coarse(const ProbParams& pp, const StepCoefs& sc, const double* x0, double* nodes,
+                    double* g_prev, const double* fine, int m, long long sub, int mode,
+                    cudaStream_t st);
+template <class P, int KIND, int S>
 int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
                       const double* X_local, long long n, long long offset, double* record,
                       void* ws, size_t ws_bytes, cudaStream_t st);
@@ -119,6 +123,25 @@ struct SeqFn {
     int operator()() {
         return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
             return seq_march<Q, K, SS>(*pp, *sc, tol, max_inner, x0, X, B, N, status, st);
+        });
+    }
+};
+
+struct PararealFn {
+    const odx_stepper* S;
+    const ProbParams* pp;
+    const StepCoefs* sc;
+    const double* x0;
+    double *nodes, *g_prev;
+    const double* fine;
+    int m;
+    long long sub;
+    int mode;
+    cudaStream_t st;
+    template <class PP>
+    int operator()() {
+        return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
+            return parareal_coarse<Q, K, SS>(*pp, *sc, x0, nodes, g_prev, fine, m, sub, mode, st);
         });
     }
 };
@@ -308,6 +331,24 @@ int odx_seq_march(const odx_problem* P, const odx_stepper* S, const double* x0, 
     if (N == 0) return ODX_OK;
     SeqFn fn{S, &pp, &sc, tol, max_inner, x0, X, B, N, reinterpret_cast<long long*>(status),
              (cudaStream_t)stream};
+    return with_small_problem(P->problem_id, P->dim, fn);
+}
+
+int odx_parareal_coarse(const odx_problem* P, const odx_stepper* S_coarse, const double* x0,
+                        double* nodes, double* g_prev, const double* fine, int32_t m,
+                        int64_t sub, double dt_coarse, int32_t mode, void* stream) {
+    g_err.clear();
+    int rc = check_problem(P, S_coarse);
+    if (rc) return rc;
+    if (P->dim > 4) return fail(ODX_EUNSUPPORTED, "parareal supports d <= 4");
+    if (S_coarse->kind != ODX_STEP_EXPLICIT_RK) return fail(ODX_EINVAL, "coarse stepper must be explicit");
+    if (!x0 || !nodes || !g_prev || m < 1 || (mode == 1 && (!fine || sub < 1)) || mode < 0 || mode > 1)
+        return fail(ODX_EINVAL, "bad parareal buffers or extents");
+    ProbParams pp;
+    StepCoefs sc;
+    if (!fill_params(P, pp)) return fail(ODX_EINVAL, "bad problem parameters");
+    if (!fill_coefs(S_coarse, dt_coarse, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
+    PararealFn fn{S_coarse, &pp, &sc, x0, nodes, g_prev, fine, m, sub, mode, (cudaStream_t)stream};
     return with_small_problem(P->problem_id, P->dim, fn);
 }
 

@@ -122,6 +122,72 @@ __global__ void seq_implicit_kernel(ProbParams pp, StepCoefs sc, double tol, int
     status[b] = st;
 }
 
+// Parareal's sequential coarse sweep (baselines.solve_parareal :164-227), one
+// thread: mode 0 initialises the nodes with the coarse propagator G (one
+// explicit step of dt_coarse per interval); mode 1 applies the correction
+//   nodes[k+1] <- G(nodes[k]^new) + F(nodes[k]^old) - G(nodes[k]^old)
+// with F = the last state of interval k's fine pass (fine: m x sub x d).
+template <class P, int S>
+__global__ void parareal_coarse_kernel(ProbParams pp, StepCoefs sc, const double* x0,
+                                       double* nodes, double* g_prev, const double* fine, int m,
+                                       long long sub, int mode) {
+    constexpr int D = P::D;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const P prob(pp);
+    double x[D];
+#pragma unroll
+    for (int r = 0; r < D; r++) {
+        x[r] = x0[r];
+        nodes[r] = x0[r];
+    }
+    for (int k = 0; k < m; k++) {
+        double kap[S][D];
+#pragma unroll
+        for (int i = 0; i < S; i++) {
+            double xs[D];
+#pragma unroll
+            for (int r = 0; r < D; r++) {
+                double acc = x[r];
+#pragma unroll
+                for (int j = 0; j < i; j++) acc += sc.dta[i * S + j] * kap[j][r];
+                xs[r] = acc;
+            }
+            prob.f(xs, kap[i]);
+        }
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < S; i++) acc += sc.b[i] * kap[i][r];
+            const double g = x[r] + sc.dt * acc;  // G(x) = x + coarse increment
+            double nxt;
+            if (mode == 0) {
+                nxt = g;
+            } else {
+                const double fe = fine[((long long)k * sub + (sub - 1)) * D + r];
+                nxt = g + fe - g_prev[k * D + r];
+            }
+            g_prev[k * D + r] = g;
+            nodes[(k + 1) * D + r] = nxt;
+            x[r] = nxt;
+        }
+    }
+}
+
+template <class P, int KIND, int S>
+int parareal_coarse(const ProbParams& pp, const StepCoefs& sc, const double* x0, double* nodes,
+                    double* g_prev, const double* fine, int m, long long sub, int mode,
+                    cudaStream_t st) {
+    if constexpr (KIND != 0) {
+        return fail(ODX_EINVAL, "parareal needs an explicit coarse stepper");
+    } else {
+        parareal_coarse_kernel<P, S><<<1, 32, 0, st>>>(pp, sc, x0, nodes, g_prev, fine, m, sub, mode);
+        ODX_CUDA(cudaGetLastError());
+        count_launch(1);
+        return ODX_OK;
+    }
+}
+
 template <class P, int KIND, int S>
 int seq_march(const ProbParams& pp, const StepCoefs& sc, double tol, int max_inner,
               const double* x0, double* X, long long B, long long N, long long* status,

@@ -671,3 +671,64 @@ def test_sequential_errors_and_batch(pkg, oracle):
     for b in range(3):
         ref = oracle.seq_explicit(1, (1.0,), oracle.RK4_A, oracle.RK4_B, x0s[b], 1e-3, 5000)
         scaled_close(Xb[b], ref, 1e-9, f"batch {b}")
+
+
+def _parareal_host(oracle, pid, params, prob, coarse_a, coarse_b, cfg):
+    """solve_parareal (baselines.py:164-227) restated on the host for the test:
+    fine passes with the oracle's seq_explicit, coarse steps x + eval(x, dt)."""
+    m, sub, d = cfg.n_coarse, cfg.fine_substeps, prob.dim
+    span = prob.tf - prob.t0
+    dtc, dtf = span / m, span / cfg.n_fine_total
+    s = len(coarse_b)
+
+    def G(x):
+        kap = np.empty((s, d))
+        for i in range(s):
+            xs = x.copy()
+            for j in range(i):
+                xs += dtc * coarse_a[i, j] * kap[j]
+            kap[i] = prob.f(xs)
+        g = np.zeros(d)
+        for i in range(s):
+            g += coarse_b[i] * kap[i]
+        return x + dtc * g
+    nodes = np.empty((m + 1, d))
+    nodes[0] = prob.x0
+    gp = np.empty((m, d))
+    for k in range(m):
+        gp[k] = G(nodes[k])
+        nodes[k + 1] = gp[k]
+    hist = [nodes.copy()]
+    fine = None
+    for _ in range(cfg.n_iterations):
+        fine = np.stack([oracle.seq_explicit(pid, params, oracle.RK4_A, oracle.RK4_B, nodes[k], dtf,
+                                             sub) for k in range(m)])
+        new = np.empty_like(nodes)
+        new[0] = prob.x0
+        for k in range(m):
+            gk = G(new[k])
+            new[k + 1] = gk + fine[k, -1] - gp[k]
+            gp[k] = gk
+        nodes = new
+        hist.append(nodes.copy())
+    return nodes, fine.reshape(-1, d), hist
+
+
+def test_parareal_vs_host_restatement(pkg, oracle):
+    """solve_parareal on the GPU (coarse Euler, fine RK4, VdP mu=1) against the
+    reference algorithm restated on the host over the oracle's marchers:
+    node history, final nodes and fine trajectory."""
+    prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=8.0)
+    coarse = pkg.get_stepper("euler", prob)
+    fine = pkg.get_stepper("rk4", prob)
+    cfg = pkg.PararealConfig(n_coarse=40, n_iterations=4, fine_substeps=50)
+    res = pkg.solve_parareal(prob, coarse, fine, cfg)
+    nodes, traj, hist = _parareal_host(oracle, 1, (1.0,), prob, np.zeros((1, 1)), np.ones(1), cfg)
+    assert len(res.node_history) == len(hist) == cfg.n_iterations + 1
+    for r, (a, b) in enumerate(zip(res.node_history, hist)):
+        scaled_close(a, b, 1e-9, f"round {r} nodes")
+    scaled_close(res.coarse_nodes, nodes, 1e-9, "final nodes")
+    scaled_close(res.trajectory.states, traj, 1e-9, "fine trajectory")
+    assert res.trajectory.n_steps == cfg.n_fine_total
+    with pytest.raises(ValueError):
+        pkg.solve_parareal(prob, pkg.get_stepper("backward_euler", prob), fine, cfg)
