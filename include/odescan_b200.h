@@ -210,7 +210,15 @@ int odx_add_inplace(double* X, const double* U, int64_t n, int32_t d, void* stre
  *                    X_local += Fp_k z + cp_k, *step_out = max|dx| (NaN-ignoring),
  *                    and halo += carry (rank r-1's last dx, bit-identical), so
  *                    the halo needs no second exchange.
- * The workspace must be the same buffer for both calls of an iteration.       */
+ *   odx_shard_step   odx_shard_fixup of iteration it fused with
+ *                    odx_shard_local of iteration it+1: one pass over the
+ *                    rank's steps applies the update and builds the next
+ *                    elements while the new rows are in registers.  The
+ *                    record's step_prev slot is filled (this rank's max|dx|).
+ *                    Protocol: local once, then per continuing iteration:
+ *                    all-gather, decide, step.  Requires a preceding local or
+ *                    step on the same workspace.
+ * The workspace must be the same buffer for all calls of a solve.            */
 #define ODX_SHARD_REC(d) ((d) * (d) + 2 * (d) + 4)
 size_t odx_shard_workspace_bytes(const odx_problem* P, const odx_stepper* S,
                                  int64_t N_local);
@@ -222,6 +230,10 @@ int odx_shard_fixup(const odx_problem* P, const double* records, int32_t rank,
                     int32_t nranks, double* X_local, int64_t N_local, double* halo,
                     double* step_out, void* workspace, size_t workspace_bytes,
                     void* stream);
+int odx_shard_step(const odx_problem* P, const odx_stepper* S, const double* records,
+                   int32_t rank, int32_t nranks, double* halo, double* X_local,
+                   int64_t N_local, int64_t offset, double dt, double* record,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

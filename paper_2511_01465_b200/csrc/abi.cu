@@ -35,7 +35,7 @@ int parareal_coarse(const ProbParams& pp, const StepCoefs& sc, const double* x0,
 template <class P, int KIND, int S>
 int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
                       const double* X_local, long long n, long long offset, double* record,
-                      void* ws, size_t ws_bytes, cudaStream_t st);
+                      void* ws, size_t ws_bytes, cudaStream_t st, int fused);
 int scan_op(const double* F, const double* c, long long N, int d, double* Fp, double* cp,
             void* ws, size_t ws_bytes, cudaStream_t st);
 size_t scan_op_ws(long long N, int d);
@@ -156,10 +156,12 @@ struct ShardLocalFn {
     void* ws;
     size_t ws_bytes;
     cudaStream_t st;
+    int fused;
     template <class PP>
     int operator()() {
         return with_stepper<PP>(S, [&]<class Q, int K, int SS>() {
-            return shard_tiled_local<Q, K, SS>(*pp, *sc, halo, X, n, offset, record, ws, ws_bytes, st);
+            return shard_tiled_local<Q, K, SS>(*pp, *sc, halo, X, n, offset, record, ws, ws_bytes, st,
+                                               fused);
         });
     }
 };
@@ -302,12 +304,12 @@ int build_common_offset(const odx_problem* P, const odx_stepper* S, int kind, co
 // one rank's local pass of the time-sharded iteration (shard.cu validates)
 int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
                          const double* halo, const double* X_local, long long n, long long offset,
-                         double* record, void* ws, size_t ws_bytes, cudaStream_t st) {
+                         double* record, void* ws, size_t ws_bytes, cudaStream_t st, int fused) {
     ProbParams pp;
     StepCoefs sc;
     if (!fill_params(P, pp)) return fail(ODX_EINVAL, "bad problem parameters");
     if (!fill_coefs(S, dt, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
-    ShardLocalFn fn{S, &pp, &sc, halo, X_local, n, offset, record, ws, ws_bytes, st};
+    ShardLocalFn fn{S, &pp, &sc, halo, X_local, n, offset, record, ws, ws_bytes, st, fused};
     return with_small_problem(P->problem_id, P->dim, fn);
 }
 }  // namespace odx

@@ -13,6 +13,10 @@
 //                     max|dx| -> step; the last row is set to x_last + A_r(z_r)
 //                     and halo += z_r, both from the same affine map, so the
 //                     halo is bit-identical to rank r-1's new last row.
+//   odx_shard_step  : fixup + the next iteration's local in one pass over the
+//                     rank's steps (shard_tiled.cuh: shard_fused_kernel); the
+//                     carry pass below precomputes every chunk's incoming
+//                     update state with the same affine map.
 #include <climits>
 #include <cstring>
 
@@ -23,7 +27,7 @@ namespace odx {
 
 int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
                          const double* halo, const double* X_local, long long n, long long offset,
-                         double* record, void* ws, size_t ws_bytes, cudaStream_t st);
+                         double* record, void* ws, size_t ws_bytes, cudaStream_t st, int fused);
 int dense_supported(const odx_problem* P, const odx_stepper* S);
 
 // out = F z + c.  One non-inlined function for the carry, the exit state and
@@ -68,6 +72,67 @@ __global__ void shard_finish_kernel(const double* recs, int rank, int d, const d
     const double* xl = recs + (long long)rank * ODX_SHARD_REC(d) + d * d + d;
     if (t < d) X[(n - 1) * d + t] = xl[t] + dlast[t];
     if (t == 0 && step_out) *step_out = bitsd(red[2]);
+}
+
+// fused step: carry z of `rank` from the gathered records, halo += z, then
+// per chunk c: zc[c] = A_cpre[c](z) (zc[nch] is the rank's exit state) and the
+// new state before chunk c's first step: the new halo (c = 0) or bnd[c] + zc[c]
+template <int D>
+__global__ void shard_step_carry_kernel(const double* recs, int rank, const double* cpre, int nch,
+                                        const double* bnd, double* halo, double* zc,
+                                        double* prevs) {
+    constexpr int E = D * D + D;
+    __shared__ double s_z[4], s_h[4];
+    if (threadIdx.x == 0) {
+        const int R = ODX_SHARD_REC(D);
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < rank; q++) {
+            const double* F = recs + (long long)q * R;
+            double t[4];
+            affine_apply(F, F + D * D, v, D, t);
+            for (int r = 0; r < D; r++) v[r] = t[r];
+        }
+        for (int r = 0; r < D; r++) {
+            s_z[r] = v[r];
+            double h = halo[r];
+            if (rank > 0) {
+                h = h + v[r];
+                halo[r] = h;
+            }
+            s_h[r] = h;
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c <= nch; c += blockDim.x) {
+        const double* A = cpre + (long long)c * E;
+        double e[4];
+        affine_apply(A, A + D * D, s_z, D, e);
+        for (int j = 0; j < D; j++) {
+            zc[c * D + j] = e[j];
+            if (c < nch) prevs[c * D + j] = (c == 0) ? s_h[j] : bnd[c * D + j] + e[j];
+        }
+    }
+}
+
+template <int D>
+int shard_step_d(const odx_problem* P, const odx_stepper* S, const double* records, int rank,
+                 double* halo, double* X_local, long long n, long long offset, double dt,
+                 double* record, void* ws, size_t ws_bytes, cudaStream_t st) {
+    constexpr int THREADS = 128, ITEMS = (D <= 2) ? 4 : 2;
+    constexpr long long T = (long long)THREADS * ITEMS;
+    const int nch_max = shard_chunks();
+    const ShardTiledLayout<D> lay(n, nch_max);
+    if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "shard workspace");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    const long long ntiles = (n + T - 1) / T;
+    const int nch = (int)(ntiles < nch_max ? ntiles : nch_max);
+    shard_step_carry_kernel<D><<<1, 320, 0, st>>>(
+        records, rank, reinterpret_cast<const double*>(base + lay.cpre), nch,
+        reinterpret_cast<const double*>(base + lay.bnd), halo,
+        reinterpret_cast<double*>(base + lay.zc), reinterpret_cast<double*>(base + lay.prevs));
+    ODX_CUDA(cudaGetLastError());
+    count_launch(1);
+    return shard_local_dispatch(P, S, dt, halo, X_local, n, offset, record, ws, ws_bytes, st, 1);
 }
 
 template <int D>
@@ -145,7 +210,22 @@ int odx_shard_local(const odx_problem* P, const odx_stepper* S, const double* ha
     if (N_local < 1 || offset < 0) return fail(ODX_EINVAL, "bad shard extent");
     if (!halo || !X_local || !record) return fail(ODX_EINVAL, "null device buffer");
     return shard_local_dispatch(P, S, dt, halo, X_local, N_local, offset, record, workspace,
-                                workspace_bytes, (cudaStream_t)stream);
+                                workspace_bytes, (cudaStream_t)stream, 0);
+}
+
+int odx_shard_step(const odx_problem* P, const odx_stepper* S, const double* records, int32_t rank,
+                   int32_t nranks, double* halo, double* X_local, int64_t N_local, int64_t offset,
+                   double dt, double* record, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+    if (!P || !S || P->dim < 1 || P->dim > 4 || dense_supported(P, S))
+        return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
+    if (rank < 0 || rank >= nranks || N_local < 1 || offset < 0)
+        return fail(ODX_EINVAL, "bad rank / extent");
+    if (!records || !halo || !X_local || !record) return fail(ODX_EINVAL, "null device buffer");
+    return with_dim(P->dim, [&]<int D>() {
+        return shard_step_d<D>(P, S, records, rank, halo, X_local, N_local, offset, dt, record,
+                               workspace, workspace_bytes, (cudaStream_t)stream);
+    });
 }
 
 int odx_shard_fixup(const odx_problem* P, const double* records, int32_t rank, int32_t nranks,

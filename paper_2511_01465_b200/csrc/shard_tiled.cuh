@@ -9,9 +9,14 @@
 //            A_r(z_r) with ONE non-inlined affine map, K3 apply with the carry,
 //            then the last row is set from the exit state — bit-identical to
 //            what rank r+1 adds to its halo — and halo += z_r.
+//   step   : fixup of iteration it fused with local of iteration it+1 in ONE
+//            pass over the rank's steps (shard_fused_kernel): each tile's old
+//            elements and rows are scanned into the new rows, which are built
+//            into the new elements while still in registers; the elements and
+//            rows cross HBM once per iteration instead of twice.
 //
-// The rank's elements stay in its workspace between the two calls: one build
-// per iteration, no look-back, one collective.
+// The rank's elements stay in its workspace between the calls: one build per
+// iteration, no look-back, one collective.
 #pragma once
 
 #include "solve_tiled.cuh"
@@ -24,7 +29,7 @@ template <int D>
 struct ShardTiledLayout {
     static constexpr int E = D * D + D;
     static constexpr int T = 512;  // THREADS (128) x ITEMS (4) for d <= 2; d >= 3 uses 256
-    size_t red, stop, z, dlast, el, cagg, cpre, total;
+    size_t red, stop, z, dlast, el, cagg, cpre, zc, prevs, bnd, total;
     ShardTiledLayout(long long n, int nch) {
         size_t off = 0;
         auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
@@ -35,16 +40,30 @@ struct ShardTiledLayout {
         el = at((size_t)n * E * 8);
         cagg = at((size_t)nch * E * 8);
         cpre = at(((size_t)nch + 1) * E * 8);
+        zc = at(((size_t)nch + 1) * D * 8);     // chunk incoming update states
+        prevs = at(((size_t)nch + 1) * D * 8);  // new state before each chunk
+        bnd = at(((size_t)nch + 1) * D * 8);    // [c] = row before chunk c
         total = off + 256;
     }
 };
 
+// the record; step_prev = this pass's max|dx| when it applied an update
+// (fused), else NaN (the caller stores it).  Non-fused passes also record the
+// row before each chunk (bnd) for the next fused pass.
 template <int D>
 __global__ void shard_tiled_record_kernel(const double* cpre_range, const double* X, long long n,
                                           const unsigned long long* red, int explicit_kind,
-                                          double* rec) {
+                                          int fused, double* bnd, long long rows_per_chunk,
+                                          int nch, double* rec) {
     const int t = threadIdx.x;
     constexpr int dd = D * D;
+    if (!fused)
+        for (int c = 1 + t; c < nch; c += 32) {
+            const long long k0 = (long long)c * rows_per_chunk;
+            if (k0 < n)
+#pragma unroll
+                for (int j = 0; j < D; j++) bnd[c * D + j] = X[(k0 - 1) * D + j];
+        }
     if (t < dd) rec[t] = cpre_range[t];
     if (t < D) {
         rec[dd + t] = cpre_range[dd + t];
@@ -54,15 +73,284 @@ __global__ void shard_tiled_record_kernel(const double* cpre_range, const double
         const double rn = bitsd(red[0]);
         rec[dd + 2 * D + 0] = rn;
         rec[dd + 2 * D + 1] = explicit_kind ? rn : bitsd(red[1]);
-        rec[dd + 2 * D + 2] = __longlong_as_double(0x7ff8000000000000ll);  // step_prev: caller
+        rec[dd + 2 * D + 2] = fused ? bitsd(red[2]) : __longlong_as_double(0x7ff8000000000000ll);
         rec[dd + 2 * D + 3] = (red[3] == ~0ull) ? -1.0 : (double)(long long)red[3];
+    }
+}
+
+
+struct ShardFusedParams {
+    ProbParams prob;
+    StepCoefs sc;
+    double* X;             // n x d rows: old in, new out (in place)
+    double* el;            // n x E elements: old in, new out (in place)
+    double* cagg;          // nch x E new chunk aggregates
+    const double* zc;      // (nch + 1) x d: update state entering chunk c (old scan)
+    const double* prevs;   // nch x d: new state before chunk c's first step
+    double* bnd;           // (nch + 1) x d: new last row of chunk c-1 at [c]
+    unsigned long long* red;
+    long long n, offset, ntiles;
+    int nch;
+};
+
+template <int D, int THREADS, int ITEMS>
+struct ShardFusedSmem {
+    static constexpr int E = D * D + D, T = THREADS * ITEMS;
+    double el[2][T * E];
+    double x[2][T * D];
+    double out[T * E];
+    uint64_t bar[2];
+};
+
+// CTA c walks its chunk in order.  Per tile: old elements + old rows (TMA,
+// double-buffered) -> block scan with the running update state -> new rows
+// (X += dx, written in place); the chunk's last row is instead set to
+// x_old + zc[c+1], the same value the next chunk's CTA derives for its first
+// step's predecessor (prevs) — so every step is built against exactly the row
+// stored.  The new rows are then built into the new elements (build_step),
+// staged in smem, written over the old ones, and folded into the chunk
+// aggregate; rn / sc / first singular step / max|dx| -> red.
+template <class P, int KIND, int S, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) shard_fused_kernel(const ShardFusedParams fp) {
+    constexpr int D = P::D, E = D * D + D, NW = THREADS / 32, T = THREADS * ITEMS;
+    using SM = ShardFusedSmem<D, THREADS, ITEMS>;
+    extern __shared__ __align__(16) unsigned char fused_raw[];
+    SM& sm = *reinterpret_cast<SM*>(fused_raw);
+    __shared__ double s_wt[NW][E];
+    __shared__ int s_wh[NW];
+    __shared__ double s_nt[NW][E];
+    __shared__ int s_nh[NW];
+    __shared__ double s_z[D];
+    __shared__ double s_prev[D];
+    __shared__ double s_wl[NW][D];
+    __shared__ double s_rd[3][NW];
+    __shared__ unsigned long long s_rb[NW];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const P prob(fp.prob);
+    const long long N = fp.n;
+    const int c = blockIdx.x;
+    long long t0, t1;
+    chunk_tiles(fp.ntiles, fp.nch, c, t0, t1);
+    const long long klast = (t1 * T < N ? t1 * T : N) - 1;
+    auto stage = [&](long long t, int b) {
+        const long long base = t * T;
+        const long long rows = (N - base) < T ? (N - base) : T;
+        const uint32_t be = (uint32_t)(rows * E * 8) & ~15u, bx = (uint32_t)(rows * D * 8) & ~15u;
+        mbar_arrive_expect_tx(&sm.bar[b], be + bx);
+        if (be) tma_load_1d(sm.el[b], fp.el + base * E, be, &sm.bar[b]);
+        if (bx) tma_load_1d(sm.x[b], fp.X + base * D, bx, &sm.bar[b]);
+    };
+    if (tid == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_global();
+        if (t0 < t1) stage(t0, 0);
+        if (t0 + 1 < t1) stage(t0 + 1, 1);
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            s_z[j] = fp.zc[c * D + j];
+            s_prev[j] = fp.prevs[c * D + j];
+        }
+    }
+    double zn[D];
+#pragma unroll
+    for (int j = 0; j < D; j++) zn[j] = fp.zc[(c + 1) * D + j];
+    __syncthreads();
+    uint32_t ph[2] = {0u, 0u};
+    double step = 0.0, rn = 0.0, scn = 0.0;
+    unsigned long long bad = ~0ull;
+    Elem<D> chunk;
+    bool chunk_has = false;
+    for (long long t = t0; t < t1; t++) {
+        const int b = (int)((t - t0) & 1);
+        const long long base = t * T;
+        const long long rows = (N - base) < T ? (N - base) : T;
+        mbar_wait(&sm.bar[b], ph[b]);
+        ph[b] ^= 1u;
+        double xn[ITEMS][D], zt[D];
+        {
+            Elem<D> el[ITEMS];
+            Elem<D> agg;
+            bool has = false;
+            const uint32_t be = (uint32_t)(rows * E * 8) & ~15u, bx = (uint32_t)(rows * D * 8) & ~15u;
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) {
+                const int r = tid * ITEMS + q;
+                if (r < rows) {
+                    if ((uint32_t)(r + 1) * E * 8 <= be)
+                        ld_elem<D>(&sm.el[b][r * E], el[q]);
+                    else
+                        ld_elem<D>(fp.el + (base + r) * E, el[q]);
+#pragma unroll
+                    for (int j = 0; j < D; j++)
+                        xn[q][j] = ((uint32_t)(r * D + j + 1) * 8 <= bx) ? sm.x[b][r * D + j]
+                                                                         : fp.X[(base + r) * D + j];
+                    if (has)
+                        compose<D>(agg, el[q], agg);
+                    else {
+                        agg = el[q];
+                        has = true;
+                    }
+                }
+            }
+            Elem<D> inc = agg;
+            bool ih = has;
+            if (!ih) set_identity<D>(inc);
+            warp_inclusive_scan<D>(inc, ih, lane);
+            if (lane == 31) {
+                st_elem<D>(s_wt[w], inc);
+                s_wh[w] = ih ? 1 : 0;
+            }
+            __syncthreads();
+            if (tid == 0 && t + 2 < t1) {
+                fence_proxy_async_smem();
+                stage(t + 2, b);
+            }
+            double z[D];
+#pragma unroll
+            for (int j = 0; j < D; j++) z[j] = s_z[j];
+            for (int q = 0; q < w; q++) {
+                if (!s_wh[q]) continue;
+                Elem<D> a;
+                ld_elem<D>(s_wt[q], a);
+                apply<D>(a, z, z);
+            }
+            Elem<D> lx;
+            shfl_up_elem<D>(inc, lx, 1);
+            const bool lxh = __shfl_up_sync(FULL, ih, 1) && lane > 0;
+            if (lxh) apply<D>(lx, z, z);
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) {
+                const long long k = base + (long long)tid * ITEMS + q;
+                if (k < N) {
+                    double dx[D];
+                    apply<D>(el[q], z, dx);
+                    step = nan_drop_max(step, row_max_abs<D>(dx));
+#pragma unroll
+                    for (int j = 0; j < D; j++) {
+                        z[j] = dx[j];
+                        xn[q][j] = xn[q][j] + (k == klast ? zn[j] : dx[j]);
+                        fp.X[k * D + j] = xn[q][j];
+                    }
+                    if (k == klast)
+#pragma unroll
+                        for (int j = 0; j < D; j++) fp.bnd[(c + 1) * D + j] = xn[q][j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < D; j++) zt[j] = z[j];
+        }
+        double pin[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) pin[j] = s_prev[j];
+        if (lane == 31)
+#pragma unroll
+            for (int j = 0; j < D; j++) s_wl[w][j] = xn[ITEMS - 1][j];
+        __syncthreads();  // (1) s_wl published, s_prev read
+        double p0[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            const double up = __shfl_up_sync(FULL, xn[ITEMS - 1][j], 1);
+            p0[j] = (tid == 0) ? pin[j] : (lane == 0 ? s_wl[w - 1][j] : up);
+        }
+        Elem<D> nagg;
+        bool nh = false;
+#pragma unroll
+        for (int q = 0; q < ITEMS; q++) {
+            const long long k = base + (long long)tid * ITEMS + q;
+            if (k < N) {
+                double prev[D], h[D];
+#pragma unroll
+                for (int j = 0; j < D; j++) prev[j] = (q == 0) ? p0[j] : xn[q - 1][j];
+                Elem<D> e;
+                const bool sing =
+                    build_step<P, KIND, S>(prob, fp.sc, prev, xn[q], fp.offset + k == 0, e, h);
+                rn = nan_drop_max(rn, row_max_abs<D>(h));
+                if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
+                if (sing && (unsigned long long)(fp.offset + k) < bad)
+                    bad = (unsigned long long)(fp.offset + k);
+                st_elem<D>(&sm.out[(tid * ITEMS + q) * E], e);
+                if (nh)
+                    compose<D>(nagg, e, nagg);
+                else {
+                    nagg = e;
+                    nh = true;
+                }
+            }
+        }
+        if (!nh) set_identity<D>(nagg);
+        warp_reduce_earliest_first<D>(nagg, nh, lane);
+        if (lane == 0) {
+            st_elem<D>(s_nt[w], nagg);
+            s_nh[w] = nh ? 1 : 0;
+        }
+        if (tid == (int)((rows - 1) / ITEMS)) {  // the tile's last step: next tile's states
+            const int ql = (int)((rows - 1) % ITEMS);
+#pragma unroll
+            for (int j = 0; j < D; j++) s_z[j] = zt[j];
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++)
+                if (q == ql)
+#pragma unroll
+                    for (int j = 0; j < D; j++) s_prev[j] = xn[q][j];
+        }
+        __syncthreads();  // (2) new elements staged, tile aggregates published
+        {
+            const int nd = (int)(rows * E);
+            double* dst = fp.el + base * E;
+            for (int q = tid; q < nd; q += THREADS) dst[q] = sm.out[q];
+        }
+        if (tid == 0) {
+            for (int q = 0; q < NW; q++) {
+                if (!s_nh[q]) continue;
+                Elem<D> a;
+                ld_elem<D>(s_nt[q], a);
+                if (chunk_has)
+                    compose<D>(chunk, a, chunk);
+                else {
+                    chunk = a;
+                    chunk_has = true;
+                }
+            }
+        }
+        __syncthreads();  // (3) sm.out and s_nt free
+    }
+    if (tid == 0) {
+        if (!chunk_has) set_identity<D>(chunk);
+        st_elem<D>(fp.cagg + (long long)c * E, chunk);
+    }
+    rn = warp_max_nan_drop(rn);
+    scn = warp_max_nan_drop(scn);
+    step = warp_max_nan_drop(step);
+    bad = warp_min_u64(bad);
+    if (lane == 0) {
+        s_rd[0][w] = rn;
+        s_rd[1][w] = scn;
+        s_rd[2][w] = step;
+        s_rb[w] = bad;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0, cc = 0.0, st2 = 0.0;
+        unsigned long long m = ~0ull;
+        for (int q = 0; q < NW; q++) {
+            a = fmax(a, s_rd[0][q]);
+            cc = fmax(cc, s_rd[1][q]);
+            st2 = fmax(st2, s_rd[2][q]);
+            m = s_rb[q] < m ? s_rb[q] : m;
+        }
+        if (a > 0.0) atomicMax(fp.red + 0, dbits(a));
+        if (cc > 0.0) atomicMax(fp.red + 1, dbits(cc));
+        if (st2 > 0.0) atomicMax(fp.red + 2, dbits(st2));
+        if (m != ~0ull) atomicMin(fp.red + 3, m);
     }
 }
 
 template <class P, int KIND, int S>
 int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
                       const double* X_local, long long n, long long offset, double* record,
-                      void* ws, size_t ws_bytes, cudaStream_t st) {
+                      void* ws, size_t ws_bytes, cudaStream_t st, int fused) {
     constexpr int D = P::D;
     constexpr int THREADS = 128, ITEMS = (D <= 2) ? 4 : 2;
     constexpr long long T = (long long)THREADS * ITEMS;
@@ -92,11 +380,38 @@ int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* h
     tp.nchunks = nch;
     tp.decide_here = 0;
     tp.kind = KIND;
+    double* bnd = reinterpret_cast<double*>(base + lay.bnd);
     init_ws(base, lay.stop + 8, 1, st);
-    tiled_build_kernel<P, KIND, S, THREADS, ITEMS><<<(unsigned)nch, THREADS, 0, st>>>(tp, 0);
+    if (fused) {
+        // the carry pass (shard.cu) has filled zc / prevs from the gathered
+        // records and the previous pass's chunk prefixes
+        ShardFusedParams fp;
+        fp.prob = pp;
+        fp.sc = sc;
+        fp.X = const_cast<double*>(X_local);
+        fp.el = tp.el;
+        fp.cagg = tp.cagg;
+        fp.zc = reinterpret_cast<const double*>(base + lay.zc);
+        fp.prevs = reinterpret_cast<const double*>(base + lay.prevs);
+        fp.bnd = bnd;
+        fp.red = tp.sp.red;
+        fp.n = n;
+        fp.offset = offset;
+        fp.ntiles = ntiles;
+        fp.nch = nch;
+        const size_t smem = sizeof(ShardFusedSmem<D, THREADS, ITEMS>);
+        auto kf = shard_fused_kernel<P, KIND, S, THREADS, ITEMS>;
+        int occ = 0;
+        if (int rc = kernel_occupancy((const void*)kf, THREADS, smem, &occ)) return rc;
+        kf<<<(unsigned)nch, THREADS, smem, st>>>(fp);
+    } else {
+        tiled_build_kernel<P, KIND, S, THREADS, ITEMS><<<(unsigned)nch, THREADS, 0, st>>>(tp, 0);
+    }
     tiled_scan_kernel<D><<<1, 32, 0, st>>>(tp, 0);
+    const long long per = (ntiles + nch - 1) / nch;
     shard_tiled_record_kernel<D><<<1, 32, 0, st>>>(tp.cpre + (long long)nch * (D * D + D), X_local,
-                                                   n, tp.sp.red, KIND == 0, record);
+                                                   n, tp.sp.red, KIND == 0, fused, bnd, per * T,
+                                                   nch, record);
     ODX_CUDA(cudaGetLastError());
     count_launch(4);
     return ODX_OK;

@@ -91,8 +91,12 @@ class ShardedNewton:
 
     backend: .local(it) -> record (1-D array-like, rec_len(d));
              .fixup(records (R, REC) host numpy) -> None;
-             .step() -> float, max|dx| of the last fix-up on this rank.
-    gather:  record -> (R, REC) numpy (the all-gather).
+             .step() -> float, max|dx| of the last fix-up on this rank;
+             or, with backend.fused true, .advance(records) -> record: the
+             fix-up of this iteration and the local pass of the next in one
+             call, the record's step_prev slot filled by the backend.
+    gather:  (record, step_local or None) -> (R, REC) numpy (the all-gather;
+             step_local, when not None, goes into the step_prev slot).
     """
 
     def __init__(self, backend, gather, d: int, max_iters: int, residual_tol: float = 0.0,
@@ -104,13 +108,16 @@ class ShardedNewton:
     def run(self) -> dict:
         d = self.d
         i_rn, i_sc, i_step, i_bad = d * d + 2 * d, d * d + 2 * d + 1, d * d + 2 * d + 2, d * d + 2 * d + 3
+        fused = bool(getattr(self.backend, "fused", False))
         hist, shist = [], []
         step_local = math.nan
         status = idx = -1
         iters = 0
+        rec = None
         for it in range(self.max_iters + 1):
-            rec = self.backend.local(it)
-            recs = np.asarray(self.gather(rec, step_local), dtype=np.float64)
+            if it == 0 or not fused:
+                rec = self.backend.local(it)
+            recs = np.asarray(self.gather(rec, None if fused else step_local), dtype=np.float64)
             rn = _nan_max(recs[:, i_rn])
             sc = _nan_max(recs[:, i_sc])
             bads = [int(b) for b in recs[:, i_bad] if b >= 0]
@@ -124,16 +131,21 @@ class ShardedNewton:
                 shist.append(sc)
             if stop:
                 break
-            self.backend.fixup(recs)
-            step_local = self.backend.step()
+            if fused:
+                rec = self.backend.advance(recs)
+            else:
+                self.backend.fixup(recs)
+                step_local = self.backend.step()
         return dict(hist=hist, shist=shist, iters=iters, status=status, status_index=idx)
 
 
 class DeviceShard:
-    """One rank's chunk on its GPU, driven through odx_shard_local / _fixup."""
+    """One rank's chunk on its GPU, driven through odx_shard_local and either
+    odx_shard_fixup (two passes per iteration) or, with fused=True (the
+    default), odx_shard_step (one pass: update + next build)."""
 
     def __init__(self, problem, stepper, dt: float, X_local, halo, offset: int, rank: int,
-                 nranks: int):
+                 nranks: int, fused: bool = True):
         import torch
         self.torch = torch
         self.P, self.S = problem.native(), stepper.native()
@@ -152,6 +164,7 @@ class DeviceShard:
         self.step_t = torch.zeros(1, dtype=torch.float64, device=X_local.device)
         self.recs_dev = torch.empty((nranks, rec_len(d)), dtype=torch.float64,
                                     device=X_local.device)
+        self.fused = bool(fused)
 
     def local(self, it):
         N.check(N.lib().odx_shard_local(self.P, self.S, N.ptr(self.halo), N.ptr(self.X), self.n,
@@ -169,6 +182,14 @@ class DeviceShard:
     def step(self) -> float:
         return float(self.step_t.item())
 
+    def advance(self, recs_host):
+        self.recs_dev.copy_(self.torch.from_numpy(np.ascontiguousarray(recs_host)))
+        N.check(N.lib().odx_shard_step(self.P, self.S, N.ptr(self.recs_dev), self.rank,
+                                       self.nranks, N.ptr(self.halo), N.ptr(self.X), self.n,
+                                       self.offset, self.dt, N.ptr(self.rec), N.ptr(self.ws),
+                                       self.ws_bytes, N.stream_handle(self.X.device)))
+        return self.rec
+
 
 def _torch_gather(group, d, device):
     import torch
@@ -178,14 +199,16 @@ def _torch_gather(group, d, device):
     def gather(rec, step_local):
         r = rec.clone() if hasattr(rec, "clone") else torch.as_tensor(rec, dtype=torch.float64)
         r = r.to(device)
-        r[d * d + 2 * d + 2] = step_local
+        if step_local is not None:
+            r[d * d + 2 * d + 2] = step_local
         out = torch.empty((R, r.numel()), dtype=torch.float64, device=device)
         dist.all_gather_into_tensor(out, r, group=group)
         return out.cpu().numpy()
     return gather
 
 
-def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config, group=None):
+def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config, group=None,
+                       fused: bool = True):
     """Time-sharded solve of one trajectory across the ranks of `group`.
 
     X_local: this rank's (n_local, d) CUDA tensor of the initial guess (updated
@@ -205,7 +228,7 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
     dist.all_gather_into_tensor(lasts, last, group=group)
     x0 = torch.as_tensor(problem.x0, dtype=torch.float64, device=dev)
     halo = x0 if r == 0 else lasts[r - 1].clone()
-    shard = DeviceShard(problem, stepper, dt, X_local, halo, offset, r, R)
+    shard = DeviceShard(problem, stepper, dt, X_local, halo, offset, r, R, fused=fused)
     proto = ShardedNewton(shard, _torch_gather(group, d, dev), d, config.max_iters,
                           config.residual_tol, config.step_tol, config.abort_on_nonfinite)
     out = proto.run()

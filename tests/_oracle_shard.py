@@ -12,7 +12,9 @@ from oracle import oracle as O
 
 
 class OracleShard:
-    def __init__(self, pid, params, stepper, dt, X_local, halo, offset, rank, nranks):
+    def __init__(self, pid, params, stepper, dt, X_local, halo, offset, rank, nranks,
+                 fused=False):
+        self.fused = bool(fused)
         self.pid, self.params, self.stepper, self.dt = pid, params, stepper, float(dt)
         self.X = np.array(X_local, np.float64, copy=True)
         self.halo = np.array(halo, np.float64, copy=True)
@@ -47,3 +49,10 @@ class OracleShard:
 
     def step(self):
         return self._step
+
+    def advance(self, recs):
+        """fused protocol: fix-up, then the next local pass with step_prev set"""
+        self.fixup(recs)
+        rec = self.local(None)
+        rec[self.d * self.d + 2 * self.d + 2] = self._step
+        return rec

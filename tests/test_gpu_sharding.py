@@ -17,7 +17,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False):
+def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False, fused=False):
     from paper_2511_01465_b200.sharded import DeviceShard, ShardedNewton, chunk_bounds
     n, d = guess.shape
     shards = []
@@ -25,7 +25,7 @@ def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False):
         off, nl = chunk_bounds(n, R, r)
         X = torch.from_numpy(np.ascontiguousarray(guess[off:off + nl])).cuda()
         halo = torch.from_numpy(prob.x0 if r == 0 else guess[off - 1]).cuda()
-        shards.append(DeviceShard(prob, st, dt, X, halo, off, r, R))
+        shards.append(DeviceShard(prob, st, dt, X, halo, off, r, R, fused=fused))
 
     class Lockstep:
         """All R ranks behind one backend: local() of every rank, then fixups."""
@@ -43,7 +43,11 @@ def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False):
         def step(self):
             return self.steps
 
+        def advance(self, recs):
+            return [s.advance(recs).clone() for s in shards]
+
     be = Lockstep()
+    be.fused = fused
 
     def gather(recs, step_locals):
         out = torch.stack(recs).cpu().numpy()
@@ -60,14 +64,15 @@ def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False):
     ("vdp1_rk4", 1.0, "rk4", 1e-3, 20000, 10, 0.0, False),
     ("vdp10_be", 10.0, "backward_euler", 1e-3, 65536, 100, 1e-10, True),
 ])
+@pytest.mark.parametrize("fused", [False, True], ids=["two_pass", "fused"])
 @pytest.mark.parametrize("R", [2, 3, 8])
-def test_emulated_time_sharding(oracle, case, R):
+def test_emulated_time_sharding(oracle, case, R, fused):
     import paper_2511_01465_b200 as pkg
     name, mu, sname, dt, n, iters, stol, abort = case
     prob = pkg.van_der_pol(mu=mu, x0=(2.0, 0.0), tf=n * dt)
     st = pkg.get_stepper(sname, prob)
     guess = np.tile(prob.x0, (n, 1))
-    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, stol, abort)
+    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, stol, abort, fused)
     ref = oracle.solve(1, (mu,), oracle.stepper_by_name(sname), prob.x0, guess, dt, iters,
                        step_tol=stol, abort_nonfinite=abort)
     assert res["status"] == ref["status"]
@@ -113,3 +118,37 @@ def test_nccl_drivers_world_size_one(oracle):
         assert (gathered["status"] == 2).all()  # NONFINITE(1), SURVEY A.1
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["two_pass", "fused"])
+@pytest.mark.parametrize("case", [
+    # multi-tile chunks (n_local > chunks x tile): the chunk-boundary rows
+    ("vdp_long", "rk4", 1 << 20, 1e-3, 2, 4),
+    ("lorenz_be", "backward_euler", 300000, 1e-4, 3, 5),
+    ("linear4_rk4", "rk4", 700001, 1e-4, 3, 3),
+])
+def test_emulated_time_sharding_long(oracle, case, fused):
+    import paper_2511_01465_b200 as pkg
+    name, sname, n, dt, R, iters = case
+    if name == "vdp_long":
+        prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
+    elif name == "lorenz_be":
+        prob = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=n * dt)
+    else:
+        A = np.array([[-1.0, 0.5, 0.0, 0.1], [0.0, -2.0, 0.3, 0.0],
+                      [0.2, 0.0, -0.5, 0.4], [0.0, -0.1, 0.0, -1.5]])
+        from paper_2511_01465_b200.problems import linear
+        prob = linear(A, x0=(1.0, -1.0, 0.5, 2.0), tf=n * dt)
+    nat = prob.native()
+    pid, params = nat.problem_id, tuple(nat.params[:nat.n_params])
+    st = pkg.get_stepper(sname, prob)
+    guess = np.tile(prob.x0, (n, 1))
+    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, 0.0, False, fused)
+    ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), prob.x0, guess, dt, iters,
+                       abort_nonfinite=False)
+    assert res["status"] == ref["status"] and res["iters"] == ref["iters"]
+    np.testing.assert_allclose(np.array(res["hist"]), ref["hist"][:len(res["hist"])], rtol=1e-7)
+    fin = np.isfinite(ref["X"]).all(axis=1)
+    assert np.array_equal(fin, np.isfinite(X).all(axis=1))
+    scale = max(1.0, float(np.abs(ref["X"][fin]).max()))
+    assert np.abs(X[fin] - ref["X"][fin]).max() <= 1e-9 * scale

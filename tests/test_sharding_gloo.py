@@ -36,7 +36,7 @@ CASES = {
 GUESS_ONES = {"logistic_converge"}
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -50,12 +50,13 @@ def _worker(rank, world, port, case, q):
         guess = np.ones((n, x0.shape[0])) if case in GUESS_ONES else np.tile(x0, (n, 1))
         halo = x0 if rank == 0 else guess[off - 1]
         be = OracleShard(pid, params, O.stepper_by_name(sname), dt, guess[off:off + nl], halo,
-                         off, rank, world)
+                         off, rank, world, fused=fused)
         d = x0.shape[0]
 
         def gather(rec, step_local):
             r = torch.as_tensor(np.asarray(rec, np.float64).copy())
-            r[d * d + 2 * d + 2] = step_local
+            if step_local is not None:
+                r[d * d + 2 * d + 2] = step_local
             out = [torch.empty_like(r) for _ in range(world)]
             dist.all_gather(out, r)
             return torch.stack(out).numpy()
@@ -66,13 +67,14 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["two_pass", "fused"])
 @pytest.mark.parametrize("case", list(CASES))
-def test_time_sharded_protocol_gloo(oracle, case):
+def test_time_sharded_protocol_gloo(oracle, case, fused):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, fused)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

@@ -33,4 +33,11 @@ for it in range(10):
     torch.cuda.synchronize()
     t_loc.append(e[0].elapsed_time(e[1])); t_fix.append(e[1].elapsed_time(e[2]))
 print(f"R={R} n_local={n}: local {np.median(t_loc):.3f} ms, fixup {np.median(t_fix):.3f} ms, "
-      f"total {np.median(t_loc) + np.median(t_fix):.3f} ms per iteration")
+      f"total {np.median(t_loc) + np.median(t_fix):.3f} ms per iteration (two-pass)")
+t_step = []
+for it in range(13):
+    e[0].record(); sh.advance(recs); e[1].record()
+    torch.cuda.synchronize()
+    if it >= 3:
+        t_step.append(e[0].elapsed_time(e[1]))
+print(f"R={R} n_local={n}: fused step {np.median(t_step):.3f} ms per iteration")
