@@ -118,7 +118,7 @@ template <int D>
 int shard_step_d(const odx_problem* P, const odx_stepper* S, const double* records, int rank,
                  double* halo, double* X_local, long long n, long long offset, double dt,
                  double* record, void* ws, size_t ws_bytes, cudaStream_t st) {
-    constexpr int THREADS = 128, ITEMS = (D <= 2) ? 4 : 2;
+    constexpr int THREADS = SHARD_THREADS, ITEMS = shard_items<D>();
     constexpr long long T = (long long)THREADS * ITEMS;
     const int nch_max = shard_chunks();
     const ShardTiledLayout<D> lay(n, nch_max);
@@ -138,7 +138,7 @@ int shard_step_d(const odx_problem* P, const odx_stepper* S, const double* recor
 template <int D>
 int shard_fixup_d(const double* records, int rank, double* X_local, long long n, double* halo,
                   double* step_out, void* ws, size_t ws_bytes, cudaStream_t st) {
-    constexpr int THREADS = 128, ITEMS = (D <= 2) ? 4 : 2;
+    constexpr int THREADS = SHARD_THREADS, ITEMS = shard_items<D>();
     constexpr long long T = (long long)THREADS * ITEMS;
     const int nch_max = shard_chunks();
     const ShardTiledLayout<D> lay(n, nch_max);

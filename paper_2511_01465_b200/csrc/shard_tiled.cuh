@@ -23,12 +23,22 @@
 
 namespace odx {
 
-inline int shard_chunks() { return 2 * num_sms(); }
+// contiguous chunks per rank = CTAs of the build / apply / fused kernels (each
+// CTA walks its chunk's tiles in order): three per SM, the fused kernel's
+// residency for d <= 2
+inline int shard_chunks() { return 3 * num_sms(); }
+
+// tile shape of the shard kernels: 128 threads x ITEMS consecutive steps each.
+// ITEMS is odd for d <= 2 so a lane's items (ITEMS*E doubles apart in shared
+// memory) fall on distinct bank pairs up to 2-way; 3 items also leave room
+// for three CTAs per SM in the fused kernel's shared memory.
+constexpr int SHARD_THREADS = 128;
+template <int D>
+constexpr int shard_items() { return D <= 2 ? 3 : 2; }
 
 template <int D>
 struct ShardTiledLayout {
     static constexpr int E = D * D + D;
-    static constexpr int T = 512;  // THREADS (128) x ITEMS (4) for d <= 2; d >= 3 uses 256
     size_t red, stop, z, dlast, el, cagg, cpre, zc, prevs, bnd, total;
     ShardTiledLayout(long long n, int nch) {
         size_t off = 0;
@@ -111,7 +121,7 @@ struct ShardFusedSmem {
 // staged in smem, written over the old ones, and folded into the chunk
 // aggregate; rn / sc / first singular step / max|dx| -> red.
 template <class P, int KIND, int S, int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS) shard_fused_kernel(const ShardFusedParams fp) {
+__global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFusedParams fp) {
     constexpr int D = P::D, E = D * D + D, NW = THREADS / 32, T = THREADS * ITEMS;
     using SM = ShardFusedSmem<D, THREADS, ITEMS>;
     extern __shared__ __align__(16) unsigned char fused_raw[];
@@ -256,26 +266,46 @@ __global__ void __launch_bounds__(THREADS) shard_fused_kernel(const ShardFusedPa
         }
         Elem<D> nagg;
         bool nh = false;
+        auto take = [&](int q, long long k, const Elem<D>& e, const double* h, bool sing) {
+            rn = nan_drop_max(rn, row_max_abs<D>(h));
+            if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
+            if (sing && (unsigned long long)(fp.offset + k) < bad)
+                bad = (unsigned long long)(fp.offset + k);
+            st_elem<D>(&sm.out[(tid * ITEMS + q) * E], e);
+            if (nh)
+                compose<D>(nagg, e, nagg);
+            else {
+                nagg = e;
+                nh = true;
+            }
+        };
+        const long long kb = base + (long long)tid * ITEMS;
+        if (KIND == 0 && kb + ITEMS <= N) {
+            // explicit, all items present: stage-interleaved build (ILP)
+            double prev[ITEMS][D], h[ITEMS][D];
+            bool first[ITEMS];
+            Elem<D> e[ITEMS];
 #pragma unroll
-        for (int q = 0; q < ITEMS; q++) {
-            const long long k = base + (long long)tid * ITEMS + q;
-            if (k < N) {
-                double prev[D], h[D];
+            for (int q = 0; q < ITEMS; q++) {
 #pragma unroll
-                for (int j = 0; j < D; j++) prev[j] = (q == 0) ? p0[j] : xn[q - 1][j];
-                Elem<D> e;
-                const bool sing =
-                    build_step<P, KIND, S>(prob, fp.sc, prev, xn[q], fp.offset + k == 0, e, h);
-                rn = nan_drop_max(rn, row_max_abs<D>(h));
-                if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
-                if (sing && (unsigned long long)(fp.offset + k) < bad)
-                    bad = (unsigned long long)(fp.offset + k);
-                st_elem<D>(&sm.out[(tid * ITEMS + q) * E], e);
-                if (nh)
-                    compose<D>(nagg, e, nagg);
-                else {
-                    nagg = e;
-                    nh = true;
+                for (int j = 0; j < D; j++) prev[q][j] = (q == 0) ? p0[j] : xn[q - 1][j];
+                first[q] = (fp.offset + kb + q == 0);
+            }
+            build_explicit_multi<P, S, ITEMS>(prob, fp.sc, prev, xn, first, e, h);
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) take(q, kb + q, e[q], h[q], false);
+        } else {
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) {
+                const long long k = kb + q;
+                if (k < N) {
+                    double prev[D], h[D];
+#pragma unroll
+                    for (int j = 0; j < D; j++) prev[j] = (q == 0) ? p0[j] : xn[q - 1][j];
+                    Elem<D> e;
+                    const bool sing =
+                        build_step<P, KIND, S>(prob, fp.sc, prev, xn[q], fp.offset + k == 0, e, h);
+                    take(q, k, e, h, sing);
                 }
             }
         }
@@ -352,7 +382,7 @@ int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* h
                       const double* X_local, long long n, long long offset, double* record,
                       void* ws, size_t ws_bytes, cudaStream_t st, int fused) {
     constexpr int D = P::D;
-    constexpr int THREADS = 128, ITEMS = (D <= 2) ? 4 : 2;
+    constexpr int THREADS = SHARD_THREADS, ITEMS = shard_items<D>();
     constexpr long long T = (long long)THREADS * ITEMS;
     const int nch_max = shard_chunks();
     const ShardTiledLayout<D> lay(n, nch_max);

@@ -124,7 +124,7 @@ def test_nccl_drivers_world_size_one(oracle):
 @pytest.mark.parametrize("case", [
     # multi-tile chunks (n_local > chunks x tile): the chunk-boundary rows
     ("vdp_long", "rk4", 1 << 20, 1e-3, 2, 4),
-    ("lorenz_be", "backward_euler", 300000, 1e-4, 3, 5),
+    ("lorenz_be", "backward_euler", 300000, 1e-5, 3, 5),
     ("linear4_rk4", "rk4", 700001, 1e-4, 3, 3),
 ])
 def test_emulated_time_sharding_long(oracle, case, fused):
@@ -142,12 +142,24 @@ def test_emulated_time_sharding_long(oracle, case, fused):
     nat = prob.native()
     pid, params = nat.problem_id, tuple(nat.params[:nat.n_params])
     st = pkg.get_stepper(sname, prob)
-    guess = np.tile(prob.x0, (n, 1))
+    # guess: the sequential trajectory, perturbed (a constant guess over a long
+    # chaotic / oscillating horizon drives late rows to ~1e270, where 1-ulp
+    # differences are amplified past any fixed tolerance)
+    ostep = oracle.stepper_by_name(sname)
+    if sname == "rk4":
+        seq = oracle.seq_explicit(pid, params, oracle.RK4_A, oracle.RK4_B, prob.x0, dt, n)
+    else:
+        seq, _ = oracle.seq_implicit(pid, params, ostep.w_prev, ostep.w_next, prob.x0, dt, n)
+    rng = np.random.default_rng(7)
+    guess = seq * (1.0 + 1e-3 * rng.standard_normal(seq.shape))
     X, res = _emulate(pkg, prob, st, dt, guess, R, iters, 0.0, False, fused)
     ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), prob.x0, guess, dt, iters,
                        abort_nonfinite=False)
     assert res["status"] == ref["status"] and res["iters"] == ref["iters"]
-    np.testing.assert_allclose(np.array(res["hist"]), ref["hist"][:len(res["hist"])], rtol=1e-7)
+    h, hr = np.array(res["hist"]), ref["hist"][:len(res["hist"])]
+    big = hr > 1e-12  # below that the history is round-off
+    np.testing.assert_allclose(h[big], hr[big], rtol=1e-7)
+    assert (h[~big] <= 1e-12).all()
     fin = np.isfinite(ref["X"]).all(axis=1)
     assert np.array_equal(fin, np.isfinite(X).all(axis=1))
     scale = max(1.0, float(np.abs(ref["X"][fin]).max()))
