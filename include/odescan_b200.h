@@ -218,6 +218,15 @@ int odx_add_inplace(double* X, const double* U, int64_t n, int32_t d, void* stre
  *                    Protocol: local once, then per continuing iteration:
  *                    all-gather, decide, step.  Requires a preceding local or
  *                    step on the same workspace.
+ *   odx_shard_decide_step  the same step preceded by solve()'s decision for
+ *                    iteration `it`, taken ON THE DEVICE from the gathered
+ *                    records (identical on every rank): hist / scaled_hist
+ *                    [it] are written, state = {stopped, status, iterations,
+ *                    status_index} (int64, device) is set when the solve
+ *                    stops, and every later call is a no-op.  The host
+ *                    enqueues local, then per it = 0..max_iters: all-gather,
+ *                    decide_step — no host round trip per iteration; it reads
+ *                    state when it chooses to (e.g. every few iterations).
  * The workspace must be the same buffer for all calls of a solve.            */
 #define ODX_SHARD_REC(d) ((d) * (d) + 2 * (d) + 4)
 size_t odx_shard_workspace_bytes(const odx_problem* P, const odx_stepper* S,
@@ -234,6 +243,12 @@ int odx_shard_step(const odx_problem* P, const odx_stepper* S, const double* rec
                    int32_t rank, int32_t nranks, double* halo, double* X_local,
                    int64_t N_local, int64_t offset, double dt, double* record,
                    void* workspace, size_t workspace_bytes, void* stream);
+int odx_shard_decide_step(const odx_problem* P, const odx_stepper* S,
+                          const odx_newton_cfg* C, const double* records, int32_t rank,
+                          int32_t nranks, int32_t it, double* halo, double* X_local,
+                          int64_t N_local, int64_t offset, double dt, double* record,
+                          double* hist, double* scaled_hist, int64_t* state,
+                          void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@ EXPORTS = (
     "odx_solve", "odx_solve_host", "odx_initial_guess", "odx_seq_march", "odx_parareal_coarse", "odx_build_explicit", "odx_build_implicit",
     "odx_scan_affine_workspace_bytes", "odx_scan_affine", "odx_max_abs", "odx_add_inplace",
     "odx_shard_workspace_bytes", "odx_shard_local", "odx_shard_fixup", "odx_shard_step",
+    "odx_shard_decide_step",
 )
 
 
@@ -108,6 +109,9 @@ def lib():
     L.odx_shard_fixup.argtypes = [P_, vp, i32, i32, vp, i64, vp, vp, vp, sz, vp]
     L.odx_shard_step.restype = C.c_int
     L.odx_shard_step.argtypes = [P_, S_, vp, i32, i32, vp, vp, i64, i64, dbl, vp, vp, sz, vp]
+    L.odx_shard_decide_step.restype = C.c_int
+    L.odx_shard_decide_step.argtypes = [P_, S_, CFG, vp, i32, i32, i32, vp, vp,
+                                        i64, i64, dbl, vp, vp, vp, vp, vp, sz, vp]
     if L.odx_abi_version() != 1:
         raise RuntimeError("libodescan_b200 ABI version mismatch")
     _lib = L

@@ -74,35 +74,96 @@ __global__ void shard_finish_kernel(const double* recs, int rank, int d, const d
     if (t == 0 && step_out) *step_out = bitsd(red[2]);
 }
 
-// fused step: carry z of `rank` from the gathered records, halo += z, then
-// per chunk c: zc[c] = A_cpre[c](z) (zc[nch] is the rank's exit state) and the
-// new state before chunk c's first step: the new halo (c = 0) or bnd[c] + zc[c]
+// solve()'s decision on the device, from the gathered records (the same
+// reductions and order as sharded.decide / ShardedNewton.run): every rank
+// evaluates it on identical inputs, so all ranks agree without a host round
+// trip.  state = {stopped, status, iterations, status_index}.
+struct ShardDecision {
+    int max_iters, abort_nonfinite;
+    double rtol, stol;
+    double* hist;     // max_iters + 1 (may be null)
+    double* shist;
+    long long* state;
+};
+
+// carry pass of a fused step (one CTA): [decision of iteration `it`], then the
+// carry z of `rank` from the gathered records, halo += z, and per chunk c:
+// zc[c] = A_cpre[c](z) (zc[nch] is the rank's exit state) and the new state
+// before chunk c's first step: the new halo (c = 0) or bnd[c] + zc[c].
+// Resets the pass's reductions; *stop = 1 skips the rest of the step.
 template <int D>
-__global__ void shard_step_carry_kernel(const double* recs, int rank, const double* cpre, int nch,
-                                        const double* bnd, double* halo, double* zc,
-                                        double* prevs) {
-    constexpr int E = D * D + D;
+__global__ void shard_step_carry_kernel(const double* recs, int rank, int nranks, int it,
+                                        ShardDecision dec, int decide_here, const double* cpre,
+                                        int nch, const double* bnd, double* halo, double* zc,
+                                        double* prevs, unsigned long long* red, int* stop) {
+    constexpr int E = D * D + D, R = ODX_SHARD_REC(D);
     __shared__ double s_z[4], s_h[4];
+    __shared__ int s_go;
     if (threadIdx.x == 0) {
-        const int R = ODX_SHARD_REC(D);
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int q = 0; q < rank; q++) {
-            const double* F = recs + (long long)q * R;
-            double t[4];
-            affine_apply(F, F + D * D, v, D, t);
-            for (int r = 0; r < D; r++) v[r] = t[r];
-        }
-        for (int r = 0; r < D; r++) {
-            s_z[r] = v[r];
-            double h = halo[r];
-            if (rank > 0) {
-                h = h + v[r];
-                halo[r] = h;
+        int go = 1;
+        if (decide_here) {
+            if (it > 0 && dec.state[0]) {
+                go = 0;  // stopped at an earlier iteration
+            } else {
+                constexpr int i_rn = D * D + 2 * D;
+                double rn = 0.0, sc = 0.0, stp = 0.0;
+                unsigned long long bad = ~0ull;
+                for (int q = 0; q < nranks; q++) {
+                    const double* r = recs + (long long)q * R;
+                    rn = nan_drop_max(rn, r[i_rn]);
+                    sc = nan_drop_max(sc, r[i_rn + 1]);
+                    stp = nan_drop_max(stp, r[i_rn + 2]);
+                    const double b = r[i_rn + 3];
+                    if (b >= 0.0 && (unsigned long long)b < bad) bad = (unsigned long long)b;
+                }
+                SolveParams sp;
+                memset(&sp, 0, sizeof(sp));
+                sp.max_iters = dec.max_iters;
+                sp.abort_nonfinite = dec.abort_nonfinite;
+                sp.rtol = dec.rtol;
+                sp.stol = dec.stol;
+                const double step_prev = it > 0 ? stp : __longlong_as_double(0x7ff8000000000000ll);
+                const Decision d = decide(it, sp, rn, bad, step_prev);
+                if (d.status != ODX_ST_SINGULAR) {
+                    if (dec.hist) dec.hist[it] = rn;
+                    if (dec.shist) dec.shist[it] = sc;
+                }
+                if (d.stop) {
+                    dec.state[0] = 1;
+                    dec.state[1] = d.status;
+                    dec.state[2] = d.iters;
+                    dec.state[3] = d.index;
+                    go = 0;
+                } else {
+                    dec.state[0] = 0;
+                }
             }
-            s_h[r] = h;
+        }
+        s_go = go;
+        *stop = go ? 0 : 1;
+        if (go) {
+            red[0] = red[1] = red[2] = 0ull;
+            red[3] = ~0ull;
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q = 0; q < rank; q++) {
+                const double* F = recs + (long long)q * R;
+                double t[4];
+                affine_apply(F, F + D * D, v, D, t);
+                for (int r = 0; r < D; r++) v[r] = t[r];
+            }
+            for (int r = 0; r < D; r++) {
+                s_z[r] = v[r];
+                double h = halo[r];
+                if (rank > 0) {
+                    h = h + v[r];
+                    halo[r] = h;
+                }
+                s_h[r] = h;
+            }
         }
     }
     __syncthreads();
+    if (!s_go) return;
     for (int c = threadIdx.x; c <= nch; c += blockDim.x) {
         const double* A = cpre + (long long)c * E;
         double e[4];
@@ -116,8 +177,9 @@ __global__ void shard_step_carry_kernel(const double* recs, int rank, const doub
 
 template <int D>
 int shard_step_d(const odx_problem* P, const odx_stepper* S, const double* records, int rank,
-                 double* halo, double* X_local, long long n, long long offset, double dt,
-                 double* record, void* ws, size_t ws_bytes, cudaStream_t st) {
+                 int nranks, int it, const ShardDecision* dec, double* halo, double* X_local,
+                 long long n, long long offset, double dt, double* record, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
     constexpr int THREADS = SHARD_THREADS, ITEMS = shard_items<D>();
     constexpr long long T = (long long)THREADS * ITEMS;
     const int nch_max = shard_chunks();
@@ -126,10 +188,15 @@ int shard_step_d(const odx_problem* P, const odx_stepper* S, const double* recor
     char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
     const long long ntiles = (n + T - 1) / T;
     const int nch = (int)(ntiles < nch_max ? ntiles : nch_max);
-    shard_step_carry_kernel<D><<<1, 320, 0, st>>>(
-        records, rank, reinterpret_cast<const double*>(base + lay.cpre), nch,
+    ShardDecision dd;
+    std::memset(&dd, 0, sizeof(dd));
+    if (dec) dd = *dec;
+    shard_step_carry_kernel<D><<<1, 448, 0, st>>>(
+        records, rank, nranks, it, dd, dec ? 1 : 0,
+        reinterpret_cast<const double*>(base + lay.cpre), nch,
         reinterpret_cast<const double*>(base + lay.bnd), halo,
-        reinterpret_cast<double*>(base + lay.zc), reinterpret_cast<double*>(base + lay.prevs));
+        reinterpret_cast<double*>(base + lay.zc), reinterpret_cast<double*>(base + lay.prevs),
+        reinterpret_cast<unsigned long long*>(base + lay.red), reinterpret_cast<int*>(base + lay.stop));
     ODX_CUDA(cudaGetLastError());
     count_launch(1);
     return shard_local_dispatch(P, S, dt, halo, X_local, n, offset, record, ws, ws_bytes, st, 1);
@@ -223,8 +290,35 @@ int odx_shard_step(const odx_problem* P, const odx_stepper* S, const double* rec
         return fail(ODX_EINVAL, "bad rank / extent");
     if (!records || !halo || !X_local || !record) return fail(ODX_EINVAL, "null device buffer");
     return with_dim(P->dim, [&]<int D>() {
-        return shard_step_d<D>(P, S, records, rank, halo, X_local, N_local, offset, dt, record,
-                               workspace, workspace_bytes, (cudaStream_t)stream);
+        return shard_step_d<D>(P, S, records, rank, nranks, 0, nullptr, halo, X_local, N_local,
+                               offset, dt, record, workspace, workspace_bytes, (cudaStream_t)stream);
+    });
+}
+
+int odx_shard_decide_step(const odx_problem* P, const odx_stepper* S, const odx_newton_cfg* C,
+                          const double* records, int32_t rank, int32_t nranks, int32_t it,
+                          double* halo, double* X_local, int64_t N_local, int64_t offset,
+                          double dt, double* record, double* hist, double* scaled_hist,
+                          int64_t* state, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+    if (!P || !S || P->dim < 1 || P->dim > 4 || dense_supported(P, S))
+        return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
+    if (!C || C->max_iters < 1) return fail(ODX_EINVAL, "max_iters must be >= 1");
+    if (rank < 0 || rank >= nranks || N_local < 1 || offset < 0 || it < 0 || it > C->max_iters)
+        return fail(ODX_EINVAL, "bad rank / extent / iteration");
+    if (!records || !halo || !X_local || !record || !state)
+        return fail(ODX_EINVAL, "null device buffer");
+    ShardDecision dec;
+    dec.max_iters = C->max_iters;
+    dec.abort_nonfinite = C->abort_nonfinite;
+    dec.rtol = C->residual_tol;
+    dec.stol = C->step_tol;
+    dec.hist = hist;
+    dec.shist = scaled_hist;
+    dec.state = reinterpret_cast<long long*>(state);
+    return with_dim(P->dim, [&]<int D>() {
+        return shard_step_d<D>(P, S, records, rank, nranks, it, &dec, halo, X_local, N_local,
+                               offset, dt, record, workspace, workspace_bytes, (cudaStream_t)stream);
     });
 }
 

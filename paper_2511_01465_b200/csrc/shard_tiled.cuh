@@ -57,28 +57,71 @@ struct ShardTiledLayout {
     }
 };
 
-// the record; step_prev = this pass's max|dx| when it applied an update
-// (fused), else NaN (the caller stores it).  Non-fused passes also record the
+// K2 + record in one CTA (nch <= SHARD_SCAN_THREADS chunks, one per thread):
+// block scan of the chunk aggregates -> exclusive prefixes cpre[c] and the
+// range aggregate cpre[nch]; then the rank's record [range F | range c |
+// x_last | rn | sc | step_prev | bad] — step_prev is this pass's max|dx| when
+// it applied an update (fused), else NaN.  Non-fused passes also record the
 // row before each chunk (bnd) for the next fused pass.
+constexpr int SHARD_SCAN_THREADS = 512;
+
 template <int D>
-__global__ void shard_tiled_record_kernel(const double* cpre_range, const double* X, long long n,
-                                          const unsigned long long* red, int explicit_kind,
-                                          int fused, double* bnd, long long rows_per_chunk,
-                                          int nch, double* rec) {
-    const int t = threadIdx.x;
-    constexpr int dd = D * D;
-    if (!fused)
-        for (int c = 1 + t; c < nch; c += 32) {
-            const long long k0 = (long long)c * rows_per_chunk;
-            if (k0 < n)
-#pragma unroll
-                for (int j = 0; j < D; j++) bnd[c * D + j] = X[(k0 - 1) * D + j];
-        }
-    if (t < dd) rec[t] = cpre_range[t];
-    if (t < D) {
-        rec[dd + t] = cpre_range[dd + t];
-        rec[dd + D + t] = X[(n - 1) * D + t];
+__global__ void __launch_bounds__(SHARD_SCAN_THREADS)
+shard_scan_record_kernel(const double* cagg, double* cpre, int nch, const double* X, long long n,
+                         const unsigned long long* red, const int* stop, int explicit_kind,
+                         int fused, double* bnd, long long rows_per_chunk, double* rec) {
+    constexpr int E = D * D + D, dd = D * D, NW = SHARD_SCAN_THREADS / 32;
+    if (*stop) return;
+    __shared__ double s_w[NW][E];
+    __shared__ int s_wh[NW];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    Elem<D> a;
+    const bool has = t < nch;
+    if (has)
+        ld_elem<D>(cagg + (long long)t * E, a);
+    else
+        set_identity<D>(a);
+    Elem<D> inc = a;
+    bool ih = has;
+    warp_inclusive_scan<D>(inc, ih, lane);
+    if (lane == 31) {
+        st_elem<D>(s_w[w], inc);
+        s_wh[w] = ih ? 1 : 0;
     }
+    __syncthreads();
+    Elem<D> ex;
+    bool exh = false;
+    for (int q = 0; q < w; q++) {
+        if (!s_wh[q]) continue;
+        Elem<D> b;
+        ld_elem<D>(s_w[q], b);
+        if (exh)
+            compose<D>(ex, b, ex);
+        else {
+            ex = b;
+            exh = true;
+        }
+    }
+    Elem<D> lx;
+    shfl_up_elem<D>(inc, lx, 1);
+    const bool lxh = __shfl_up_sync(FULL, ih, 1) && lane > 0;
+    if (lxh) {
+        if (exh)
+            compose<D>(ex, lx, ex);
+        else {
+            ex = lx;
+            exh = true;
+        }
+    }
+    if (!exh) set_identity<D>(ex);
+    if (has) st_elem<D>(cpre + (long long)t * E, ex);
+    if (t == nch - 1) {  // the range aggregate, straight into the record too
+        Elem<D> r = a;
+        if (exh) compose<D>(ex, a, r);
+        st_elem<D>(cpre + (long long)nch * E, r);
+        st_elem<D>(rec, r);
+    }
+    if (t < D) rec[dd + D + t] = X[(n - 1) * D + t];
     if (t == 0) {
         const double rn = bitsd(red[0]);
         rec[dd + 2 * D + 0] = rn;
@@ -86,8 +129,13 @@ __global__ void shard_tiled_record_kernel(const double* cpre_range, const double
         rec[dd + 2 * D + 2] = fused ? bitsd(red[2]) : __longlong_as_double(0x7ff8000000000000ll);
         rec[dd + 2 * D + 3] = (red[3] == ~0ull) ? -1.0 : (double)(long long)red[3];
     }
+    if (!fused && t >= 1 && t < nch) {
+        const long long k0 = (long long)t * rows_per_chunk;
+        if (k0 < n)
+#pragma unroll
+            for (int j = 0; j < D; j++) bnd[t * D + j] = X[(k0 - 1) * D + j];
+    }
 }
-
 
 struct ShardFusedParams {
     ProbParams prob;
@@ -99,6 +147,7 @@ struct ShardFusedParams {
     const double* prevs;   // nch x d: new state before chunk c's first step
     double* bnd;           // (nch + 1) x d: new last row of chunk c-1 at [c]
     unsigned long long* red;
+    const int* stop;       // set by the carry / decision pass: skip the pass
     long long n, offset, ntiles;
     int nch;
 };
@@ -135,6 +184,7 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
     __shared__ double s_wl[NW][D];
     __shared__ double s_rd[3][NW];
     __shared__ unsigned long long s_rb[NW];
+    if (*fp.stop) return;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const P prob(fp.prob);
     const long long N = fp.n;
@@ -411,10 +461,11 @@ int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* h
     tp.decide_here = 0;
     tp.kind = KIND;
     double* bnd = reinterpret_cast<double*>(base + lay.bnd);
-    init_ws(base, lay.stop + 8, 1, st);
+    if (nch > SHARD_SCAN_THREADS) return fail(ODX_EUNSUPPORTED, "too many shard chunks");
     if (fused) {
-        // the carry pass (shard.cu) has filled zc / prevs from the gathered
-        // records and the previous pass's chunk prefixes
+        // the carry / decision pass (shard.cu) has reset red and stop and
+        // filled zc / prevs from the gathered records and the previous
+        // pass's chunk prefixes
         ShardFusedParams fp;
         fp.prob = pp;
         fp.sc = sc;
@@ -425,6 +476,7 @@ int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* h
         fp.prevs = reinterpret_cast<const double*>(base + lay.prevs);
         fp.bnd = bnd;
         fp.red = tp.sp.red;
+        fp.stop = tp.stop;
         fp.n = n;
         fp.offset = offset;
         fp.ntiles = ntiles;
@@ -435,15 +487,14 @@ int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* h
         if (int rc = kernel_occupancy((const void*)kf, THREADS, smem, &occ)) return rc;
         kf<<<(unsigned)nch, THREADS, smem, st>>>(fp);
     } else {
+        init_ws(base, lay.stop + 8, 1, st);
         tiled_build_kernel<P, KIND, S, THREADS, ITEMS><<<(unsigned)nch, THREADS, 0, st>>>(tp, 0);
     }
-    tiled_scan_kernel<D><<<1, 32, 0, st>>>(tp, 0);
     const long long per = (ntiles + nch - 1) / nch;
-    shard_tiled_record_kernel<D><<<1, 32, 0, st>>>(tp.cpre + (long long)nch * (D * D + D), X_local,
-                                                   n, tp.sp.red, KIND == 0, fused, bnd, per * T,
-                                                   nch, record);
+    shard_scan_record_kernel<D><<<1, SHARD_SCAN_THREADS, 0, st>>>(
+        tp.cagg, tp.cpre, nch, X_local, n, tp.sp.red, tp.stop, KIND == 0, fused, bnd, per * T, record);
     ODX_CUDA(cudaGetLastError());
-    count_launch(4);
+    count_launch(fused ? 2 : 3);
     return ODX_OK;
 }
 

@@ -182,6 +182,16 @@ class DeviceShard:
     def step(self) -> float:
         return float(self.step_t.item())
 
+    def decide_step(self, it, cfg, hist, shist, state):
+        """odx_shard_decide_step: decision of iteration `it` on the device from
+        self.recs_dev (already gathered), then the fused step if continuing."""
+        N.check(N.lib().odx_shard_decide_step(
+            self.P, self.S, cfg, N.ptr(self.recs_dev), self.rank, self.nranks, int(it),
+            N.ptr(self.halo), N.ptr(self.X), self.n, self.offset, self.dt, N.ptr(self.rec),
+            N.ptr(hist), N.ptr(shist), N.ptr(state), N.ptr(self.ws), self.ws_bytes,
+            N.stream_handle(self.X.device)))
+        return self.rec
+
     def advance(self, recs_host):
         self.recs_dev.copy_(self.torch.from_numpy(np.ascontiguousarray(recs_host)))
         N.check(N.lib().odx_shard_step(self.P, self.S, N.ptr(self.recs_dev), self.rank,
@@ -189,6 +199,43 @@ class DeviceShard:
                                        self.offset, self.dt, N.ptr(self.rec), N.ptr(self.ws),
                                        self.ws_bytes, N.stream_handle(self.X.device)))
         return self.rec
+
+
+def run_device_decided(shards, gather_into, config, poll: int = 8) -> dict:
+    """The time-sharded protocol with the decision taken on the device.
+
+    shards: the DeviceShard(s) driven by this process (one per rank; several
+    only when emulating ranks on one GPU).  gather_into(): all-gathers every
+    shard's .rec into its .recs_dev on the device (NCCL, no host sync).
+    Per iteration the host only enqueues: all-gather, decide_step.  It reads
+    the stop flag every `poll` iterations; iterations enqueued after the stop
+    are no-ops on the device.  Returns ShardedNewton.run()'s dict.
+    """
+    import torch
+    sh0 = shards[0]
+    dev = sh0.X.device
+    m = int(config.max_iters)
+    cfg = N.make_cfg(m, config.residual_tol, config.step_tol, config.abort_on_nonfinite)
+    bufs = []
+    for _ in shards:
+        bufs.append((torch.full((m + 1,), math.nan, dtype=torch.float64, device=dev),
+                     torch.full((m + 1,), math.nan, dtype=torch.float64, device=dev),
+                     torch.zeros(4, dtype=torch.int64, device=dev)))
+    for s in shards:
+        s.local(0)
+    for it in range(m + 1):
+        gather_into()
+        for s, (h, sh, st) in zip(shards, bufs):
+            s.decide_step(it, cfg, h, sh, st)
+        if it < m and (it + 1) % poll == 0 and int(bufs[0][2][0].item()):
+            break
+    h, sh, st = (b.cpu().numpy() for b in bufs[0])
+    stopped, status, iters, idx = (int(v) for v in st)
+    if not stopped:
+        raise RuntimeError("device-decided protocol did not reach a decision")
+    n_hist = iters + 1 - (1 if status == N.ST_SINGULAR else 0)
+    return dict(hist=[float(v) for v in h[:n_hist]], shist=[float(v) for v in sh[:n_hist]],
+                iters=iters, status=status, status_index=idx)
 
 
 def _torch_gather(group, d, device):
@@ -208,8 +255,12 @@ def _torch_gather(group, d, device):
 
 
 def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config, group=None,
-                       fused: bool = True):
+                       protocol: str = "device"):
     """Time-sharded solve of one trajectory across the ranks of `group`.
+
+    protocol: "device" (default) — fused passes, decision on the device, no
+    host round trip per iteration; "host" — fused passes, decision on the
+    host (ShardedNewton); "two_pass" — separate local / fix-up passes.
 
     X_local: this rank's (n_local, d) CUDA tensor of the initial guess (updated
     in place to the final iterate).  Chunks must be contiguous and ordered by
@@ -218,6 +269,8 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
     """
     import torch
     import torch.distributed as dist
+    if protocol not in ("device", "host", "two_pass"):
+        raise ValueError(f"unknown protocol {protocol!r}")
     R = dist.get_world_size(group)
     r = dist.get_rank(group)
     d = problem.dim
@@ -228,10 +281,18 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
     dist.all_gather_into_tensor(lasts, last, group=group)
     x0 = torch.as_tensor(problem.x0, dtype=torch.float64, device=dev)
     halo = x0 if r == 0 else lasts[r - 1].clone()
-    shard = DeviceShard(problem, stepper, dt, X_local, halo, offset, r, R, fused=fused)
-    proto = ShardedNewton(shard, _torch_gather(group, d, dev), d, config.max_iters,
-                          config.residual_tol, config.step_tol, config.abort_on_nonfinite)
-    out = proto.run()
+    if protocol == "device":
+        shard = DeviceShard(problem, stepper, dt, X_local, halo, offset, r, R, fused=True)
+
+        def gather_into():
+            dist.all_gather_into_tensor(shard.recs_dev, shard.rec, group=group)
+        out = run_device_decided([shard], gather_into, config)
+    else:
+        shard = DeviceShard(problem, stepper, dt, X_local, halo, offset, r, R,
+                            fused=(protocol == "host"))
+        proto = ShardedNewton(shard, _torch_gather(group, d, dev), d, config.max_iters,
+                              config.residual_tol, config.step_tol, config.abort_on_nonfinite)
+        out = proto.run()
     return TimeShardedReport(X_local=X_local, offset=offset, residual_history=out["hist"],
                              scaled_residual_history=out["shist"], iterations_run=out["iters"],
                              status=out["status"], status_index=out["status_index"])

@@ -17,8 +17,10 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False, fused=False):
-    from paper_2511_01465_b200.sharded import DeviceShard, ShardedNewton, chunk_bounds
+def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False, mode="two_pass"):
+    from paper_2511_01465_b200.sharded import (DeviceShard, ShardedNewton, chunk_bounds,
+                                               run_device_decided)
+    fused = mode != "two_pass"
     n, d = guess.shape
     shards = []
     for r in range(R):
@@ -46,6 +48,16 @@ def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False, 
         def advance(self, recs):
             return [s.advance(recs).clone() for s in shards]
 
+    if mode == "device":
+        def gather_into():
+            allrec = torch.stack([s.rec for s in shards])
+            for s in shards:
+                s.recs_dev.copy_(allrec)
+        conf = pkg.NewtonConfig(max_iters=max_iters, step_tol=step_tol, abort_on_nonfinite=abort)
+        res = run_device_decided(shards, gather_into, conf, poll=3)
+        X = np.concatenate([s.X.cpu().numpy() for s in shards])
+        return X, res
+
     be = Lockstep()
     be.fused = fused
 
@@ -64,15 +76,15 @@ def _emulate(pkg, prob, st, dt, guess, R, max_iters, step_tol=0.0, abort=False, 
     ("vdp1_rk4", 1.0, "rk4", 1e-3, 20000, 10, 0.0, False),
     ("vdp10_be", 10.0, "backward_euler", 1e-3, 65536, 100, 1e-10, True),
 ])
-@pytest.mark.parametrize("fused", [False, True], ids=["two_pass", "fused"])
+@pytest.mark.parametrize("mode", ["two_pass", "host", "device"])
 @pytest.mark.parametrize("R", [2, 3, 8])
-def test_emulated_time_sharding(oracle, case, R, fused):
+def test_emulated_time_sharding(oracle, case, R, mode):
     import paper_2511_01465_b200 as pkg
     name, mu, sname, dt, n, iters, stol, abort = case
     prob = pkg.van_der_pol(mu=mu, x0=(2.0, 0.0), tf=n * dt)
     st = pkg.get_stepper(sname, prob)
     guess = np.tile(prob.x0, (n, 1))
-    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, stol, abort, fused)
+    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, stol, abort, mode)
     ref = oracle.solve(1, (mu,), oracle.stepper_by_name(sname), prob.x0, guess, dt, iters,
                        step_tol=stol, abort_nonfinite=abort)
     assert res["status"] == ref["status"]
@@ -120,14 +132,14 @@ def test_nccl_drivers_world_size_one(oracle):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fused", [False, True], ids=["two_pass", "fused"])
+@pytest.mark.parametrize("mode", ["two_pass", "host", "device"])
 @pytest.mark.parametrize("case", [
     # multi-tile chunks (n_local > chunks x tile): the chunk-boundary rows
     ("vdp_long", "rk4", 1 << 20, 1e-3, 2, 4),
     ("lorenz_be", "backward_euler", 300000, 1e-5, 3, 5),
     ("linear4_rk4", "rk4", 700001, 1e-4, 3, 3),
 ])
-def test_emulated_time_sharding_long(oracle, case, fused):
+def test_emulated_time_sharding_long(oracle, case, mode):
     import paper_2511_01465_b200 as pkg
     name, sname, n, dt, R, iters = case
     if name == "vdp_long":
@@ -152,7 +164,7 @@ def test_emulated_time_sharding_long(oracle, case, fused):
         seq, _ = oracle.seq_implicit(pid, params, ostep.w_prev, ostep.w_next, prob.x0, dt, n)
     rng = np.random.default_rng(7)
     guess = seq * (1.0 + 1e-3 * rng.standard_normal(seq.shape))
-    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, 0.0, False, fused)
+    X, res = _emulate(pkg, prob, st, dt, guess, R, iters, 0.0, False, mode)
     ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), prob.x0, guess, dt, iters,
                        abort_nonfinite=False)
     assert res["status"] == ref["status"] and res["iters"] == ref["iters"]

@@ -22,6 +22,8 @@ halo = torch.tensor([2.0, 0.0], dtype=torch.float64, device="cuda")
 sh = DeviceShard(prob, st, dt, X, halo, offset=n * (R // 2), rank=R // 2, nranks=R)
 recs = np.zeros((R, rec_len(2)))
 recs[:, :4] = np.eye(2).ravel()
+recs[:, -4] = 1.0   # rn
+recs[:, -1] = -1.0  # no singular step
 for it in range(3):
     sh.local(it)
     sh.fixup(recs)
@@ -41,3 +43,24 @@ for it in range(13):
     if it >= 3:
         t_step.append(e[0].elapsed_time(e[1]))
 print(f"R={R} n_local={n}: fused step {np.median(t_step):.3f} ms per iteration")
+
+from paper_2511_01465_b200 import _native as N  # noqa: E402
+cfg = N.make_cfg(1000, 0.0, 0.0, False)
+hist = torch.full((1001,), float("nan"), dtype=torch.float64, device="cuda")
+shist = hist.clone()
+state = torch.zeros(4, dtype=torch.int64, device="cuda")
+sh.recs_dev.copy_(torch.from_numpy(recs))
+t_dec = []
+for it in range(1, 14):
+    e[0].record(); sh.decide_step(it, cfg, hist, shist, state); e[1].record()
+    torch.cuda.synchronize()
+    if it > 3:
+        t_dec.append(e[0].elapsed_time(e[1]))
+# back-to-back, as the device-decided protocol enqueues them (no host sync)
+e[0].record()
+for it in range(14, 34):
+    sh.decide_step(it, cfg, hist, shist, state)
+e[1].record()
+torch.cuda.synchronize()
+print(f"R={R} n_local={n}: decide+step {np.median(t_dec):.3f} ms per iteration, "
+      f"{e[0].elapsed_time(e[1]) / 20:.3f} ms back-to-back")
