@@ -227,7 +227,8 @@ int odx_add_inplace(double* X, const double* U, int64_t n, int32_t d, void* stre
  *                    enqueues local, then per it = 0..max_iters: all-gather,
  *                    decide_step — no host round trip per iteration; it reads
  *                    state when it chooses to (e.g. every few iterations).
- * The workspace must be the same buffer for all calls of a solve.            */
+ * The workspace must be the same buffer for all calls of a solve; X_local
+ * must be 16-byte aligned (it is streamed with TMA bulk copies).             */
 #define ODX_SHARD_REC(d) ((d) * (d) + 2 * (d) + 4)
 size_t odx_shard_workspace_bytes(const odx_problem* P, const odx_stepper* S,
                                  int64_t N_local);

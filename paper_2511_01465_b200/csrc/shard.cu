@@ -185,6 +185,7 @@ int shard_step_d(const odx_problem* P, const odx_stepper* S, const double* recor
     const int nch_max = shard_chunks();
     const ShardTiledLayout<D> lay(n, nch_max);
     if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "shard workspace");
+    if (reinterpret_cast<uintptr_t>(X_local) & 15) return fail(ODX_EINVAL, "X_local must be 16-byte aligned");
     char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
     const long long ntiles = (n + T - 1) / T;
     const int nch = (int)(ntiles < nch_max ? ntiles : nch_max);
@@ -276,6 +277,7 @@ int odx_shard_local(const odx_problem* P, const odx_stepper* S, const double* ha
         return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
     if (N_local < 1 || offset < 0) return fail(ODX_EINVAL, "bad shard extent");
     if (!halo || !X_local || !record) return fail(ODX_EINVAL, "null device buffer");
+    if (reinterpret_cast<uintptr_t>(X_local) & 15) return fail(ODX_EINVAL, "X_local must be 16-byte aligned");
     return shard_local_dispatch(P, S, dt, halo, X_local, N_local, offset, record, workspace,
                                 workspace_bytes, (cudaStream_t)stream, 0);
 }

@@ -137,6 +137,20 @@ shard_scan_record_kernel(const double* cagg, double* cpre, int nch, const double
     }
 }
 
+// one row of X: 16-byte stores where the row allows (torch / cudaMalloc rows
+// of d = 2, 4 doubles are 16-byte aligned)
+template <int D>
+__device__ __forceinline__ void st_row(double* dst, const double* v) {
+    if constexpr (D % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < D; j += 2)
+            *reinterpret_cast<double2*>(dst + j) = make_double2(v[j], v[j + 1]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; j++) dst[j] = v[j];
+    }
+}
+
 struct ShardFusedParams {
     ProbParams prob;
     StepCoefs sc;
@@ -233,24 +247,39 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
             Elem<D> el[ITEMS];
             Elem<D> agg;
             bool has = false;
-            const uint32_t be = (uint32_t)(rows * E * 8) & ~15u, bx = (uint32_t)(rows * D * 8) & ~15u;
+            // rows * E * 8 is a multiple of 16 (E = d(d+1) is even): the whole
+            // tile's elements are in smem; an odd tail row of X (odd d) is not
+            if (rows == T) {
 #pragma unroll
-            for (int q = 0; q < ITEMS; q++) {
-                const int r = tid * ITEMS + q;
-                if (r < rows) {
-                    if ((uint32_t)(r + 1) * E * 8 <= be)
-                        ld_elem<D>(&sm.el[b][r * E], el[q]);
+                for (int q = 0; q < ITEMS; q++) {
+                    const int r = tid * ITEMS + q;
+                    ld_elem<D>(&sm.el[b][r * E], el[q]);
+#pragma unroll
+                    for (int j = 0; j < D; j++) xn[q][j] = sm.x[b][r * D + j];
+                    if (q == 0)
+                        agg = el[0];
                     else
-                        ld_elem<D>(fp.el + (base + r) * E, el[q]);
-#pragma unroll
-                    for (int j = 0; j < D; j++)
-                        xn[q][j] = ((uint32_t)(r * D + j + 1) * 8 <= bx) ? sm.x[b][r * D + j]
-                                                                         : fp.X[(base + r) * D + j];
-                    if (has)
                         compose<D>(agg, el[q], agg);
-                    else {
-                        agg = el[q];
-                        has = true;
+                }
+                has = true;
+            } else {
+                const uint32_t bx = (uint32_t)(rows * D * 8) & ~15u;
+#pragma unroll
+                for (int q = 0; q < ITEMS; q++) {
+                    const int r = tid * ITEMS + q;
+                    if (r < rows) {
+                        ld_elem<D>(&sm.el[b][r * E], el[q]);
+#pragma unroll
+                        for (int j = 0; j < D; j++)
+                            xn[q][j] = ((uint32_t)(r * D + j + 1) * 8 <= bx)
+                                           ? sm.x[b][r * D + j]
+                                           : fp.X[(base + r) * D + j];
+                        if (has)
+                            compose<D>(agg, el[q], agg);
+                        else {
+                            agg = el[q];
+                            has = true;
+                        }
                     }
                 }
             }
@@ -280,22 +309,38 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
             shfl_up_elem<D>(inc, lx, 1);
             const bool lxh = __shfl_up_sync(FULL, ih, 1) && lane > 0;
             if (lxh) apply<D>(lx, z, z);
+            if (t + 1 < t1) {  // a full tile without the chunk's last row
 #pragma unroll
-            for (int q = 0; q < ITEMS; q++) {
-                const long long k = base + (long long)tid * ITEMS + q;
-                if (k < N) {
+                for (int q = 0; q < ITEMS; q++) {
+                    const long long k = base + (long long)tid * ITEMS + q;
                     double dx[D];
                     apply<D>(el[q], z, dx);
                     step = nan_drop_max(step, row_max_abs<D>(dx));
 #pragma unroll
                     for (int j = 0; j < D; j++) {
                         z[j] = dx[j];
-                        xn[q][j] = xn[q][j] + (k == klast ? zn[j] : dx[j]);
-                        fp.X[k * D + j] = xn[q][j];
+                        xn[q][j] = xn[q][j] + dx[j];
                     }
-                    if (k == klast)
+                    st_row<D>(fp.X + k * D, xn[q]);
+                }
+            } else {
 #pragma unroll
-                        for (int j = 0; j < D; j++) fp.bnd[(c + 1) * D + j] = xn[q][j];
+                for (int q = 0; q < ITEMS; q++) {
+                    const long long k = base + (long long)tid * ITEMS + q;
+                    if (k < N) {
+                        double dx[D];
+                        apply<D>(el[q], z, dx);
+                        step = nan_drop_max(step, row_max_abs<D>(dx));
+#pragma unroll
+                        for (int j = 0; j < D; j++) {
+                            z[j] = dx[j];
+                            xn[q][j] = xn[q][j] + (k == klast ? zn[j] : dx[j]);
+                        }
+                        st_row<D>(fp.X + k * D, xn[q]);
+                        if (k == klast)
+#pragma unroll
+                            for (int j = 0; j < D; j++) fp.bnd[(c + 1) * D + j] = xn[q][j];
+                    }
                 }
             }
 #pragma unroll
@@ -307,7 +352,8 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
         if (lane == 31)
 #pragma unroll
             for (int j = 0; j < D; j++) s_wl[w][j] = xn[ITEMS - 1][j];
-        __syncthreads();  // (1) s_wl published, s_prev read
+        if (tid == 0) tma_store_wait_read();  // the previous tile's bulk store left sm.out
+        __syncthreads();  // (1) s_wl published, s_prev read, sm.out free
         double p0[D];
 #pragma unroll
         for (int j = 0; j < D; j++) {
@@ -375,13 +421,11 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
 #pragma unroll
                     for (int j = 0; j < D; j++) s_prev[j] = xn[q][j];
         }
+        fence_proxy_async_smem();  // staged elements -> the bulk store (async proxy)
         __syncthreads();  // (2) new elements staged, tile aggregates published
-        {
-            const int nd = (int)(rows * E);
-            double* dst = fp.el + base * E;
-            for (int q = tid; q < nd; q += THREADS) dst[q] = sm.out[q];
-        }
         if (tid == 0) {
+            tma_store_1d(fp.el + base * E, sm.out, (uint32_t)(rows * E * 8));
+            tma_store_commit();
             for (int q = 0; q < NW; q++) {
                 if (!s_nh[q]) continue;
                 Elem<D> a;
@@ -394,9 +438,11 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
                 }
             }
         }
-        __syncthreads();  // (3) sm.out and s_nt free
+        // sm.out is rewritten after the next tile's sync (1), which thread 0
+        // reaches only once the bulk store has read it
     }
     if (tid == 0) {
+        tma_store_wait_all();
         if (!chunk_has) set_identity<D>(chunk);
         st_elem<D>(fp.cagg + (long long)c * E, chunk);
     }
