@@ -30,17 +30,6 @@ int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
                          double* record, void* ws, size_t ws_bytes, cudaStream_t st, int fused);
 int dense_supported(const odx_problem* P, const odx_stepper* S);
 
-// out = F z + c.  One non-inlined function for the carry, the exit state and
-// hence the halo update.
-__device__ __noinline__ void affine_apply(const double* F, const double* c, const double* z, int d,
-                                          double* out) {
-    for (int r = 0; r < d; r++) {
-        double acc = c[r];
-        for (int q = 0; q < d; q++) acc = __fma_rn(F[r * d + q], z[q], acc);
-        out[r] = acc;
-    }
-}
-
 // carry z of `rank` and its exit state dlast = A_rank(z); halo += z (rank > 0);
 // the step slot of the reduction quad is reset
 __global__ void shard_carry_kernel(const double* recs, int rank, int d, double* z, double* dlast,
@@ -72,107 +61,6 @@ __global__ void shard_finish_kernel(const double* recs, int rank, int d, const d
     const double* xl = recs + (long long)rank * ODX_SHARD_REC(d) + d * d + d;
     if (t < d) X[(n - 1) * d + t] = xl[t] + dlast[t];
     if (t == 0 && step_out) *step_out = bitsd(red[2]);
-}
-
-// solve()'s decision on the device, from the gathered records (the same
-// reductions and order as sharded.decide / ShardedNewton.run): every rank
-// evaluates it on identical inputs, so all ranks agree without a host round
-// trip.  state = {stopped, status, iterations, status_index}.
-struct ShardDecision {
-    int max_iters, abort_nonfinite;
-    double rtol, stol;
-    double* hist;     // max_iters + 1 (may be null)
-    double* shist;
-    long long* state;
-};
-
-// carry pass of a fused step (one CTA): [decision of iteration `it`], then the
-// carry z of `rank` from the gathered records, halo += z, and per chunk c:
-// zc[c] = A_cpre[c](z) (zc[nch] is the rank's exit state) and the new state
-// before chunk c's first step: the new halo (c = 0) or bnd[c] + zc[c].
-// Resets the pass's reductions; *stop = 1 skips the rest of the step.
-template <int D>
-__global__ void shard_step_carry_kernel(const double* recs, int rank, int nranks, int it,
-                                        ShardDecision dec, int decide_here, const double* cpre,
-                                        int nch, const double* bnd, double* halo, double* zc,
-                                        double* prevs, unsigned long long* red, int* stop) {
-    constexpr int E = D * D + D, R = ODX_SHARD_REC(D);
-    __shared__ double s_z[4], s_h[4];
-    __shared__ int s_go;
-    if (threadIdx.x == 0) {
-        int go = 1;
-        if (decide_here) {
-            if (it > 0 && dec.state[0]) {
-                go = 0;  // stopped at an earlier iteration
-            } else {
-                constexpr int i_rn = D * D + 2 * D;
-                double rn = 0.0, sc = 0.0, stp = 0.0;
-                unsigned long long bad = ~0ull;
-                for (int q = 0; q < nranks; q++) {
-                    const double* r = recs + (long long)q * R;
-                    rn = nan_drop_max(rn, r[i_rn]);
-                    sc = nan_drop_max(sc, r[i_rn + 1]);
-                    stp = nan_drop_max(stp, r[i_rn + 2]);
-                    const double b = r[i_rn + 3];
-                    if (b >= 0.0 && (unsigned long long)b < bad) bad = (unsigned long long)b;
-                }
-                SolveParams sp;
-                memset(&sp, 0, sizeof(sp));
-                sp.max_iters = dec.max_iters;
-                sp.abort_nonfinite = dec.abort_nonfinite;
-                sp.rtol = dec.rtol;
-                sp.stol = dec.stol;
-                const double step_prev = it > 0 ? stp : __longlong_as_double(0x7ff8000000000000ll);
-                const Decision d = decide(it, sp, rn, bad, step_prev);
-                if (d.status != ODX_ST_SINGULAR) {
-                    if (dec.hist) dec.hist[it] = rn;
-                    if (dec.shist) dec.shist[it] = sc;
-                }
-                if (d.stop) {
-                    dec.state[0] = 1;
-                    dec.state[1] = d.status;
-                    dec.state[2] = d.iters;
-                    dec.state[3] = d.index;
-                    go = 0;
-                } else {
-                    dec.state[0] = 0;
-                }
-            }
-        }
-        s_go = go;
-        *stop = go ? 0 : 1;
-        if (go) {
-            red[0] = red[1] = red[2] = 0ull;
-            red[3] = ~0ull;
-            double v[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int q = 0; q < rank; q++) {
-                const double* F = recs + (long long)q * R;
-                double t[4];
-                affine_apply(F, F + D * D, v, D, t);
-                for (int r = 0; r < D; r++) v[r] = t[r];
-            }
-            for (int r = 0; r < D; r++) {
-                s_z[r] = v[r];
-                double h = halo[r];
-                if (rank > 0) {
-                    h = h + v[r];
-                    halo[r] = h;
-                }
-                s_h[r] = h;
-            }
-        }
-    }
-    __syncthreads();
-    if (!s_go) return;
-    for (int c = threadIdx.x; c <= nch; c += blockDim.x) {
-        const double* A = cpre + (long long)c * E;
-        double e[4];
-        affine_apply(A, A + D * D, s_z, D, e);
-        for (int j = 0; j < D; j++) {
-            zc[c * D + j] = e[j];
-            if (c < nch) prevs[c * D + j] = (c == 0) ? s_h[j] : bnd[c * D + j] + e[j];
-        }
-    }
 }
 
 template <int D>

@@ -137,6 +137,118 @@ shard_scan_record_kernel(const double* cagg, double* cpre, int nch, const double
     }
 }
 
+// out = F z + c.  One non-inlined function for the carry, the exit state and
+// hence the halo update.
+static __device__ __noinline__ void affine_apply(const double* F, const double* c, const double* z, int d,
+                                          double* out) {
+    for (int r = 0; r < d; r++) {
+        double acc = c[r];
+        for (int q = 0; q < d; q++) acc = __fma_rn(F[r * d + q], z[q], acc);
+        out[r] = acc;
+    }
+}
+
+// solve()'s decision on the device, from the gathered records (the same
+// reductions and order as sharded.decide / ShardedNewton.run): every rank
+// evaluates it on identical inputs, so all ranks agree without a host round
+// trip.  state = {stopped, status, iterations, status_index}.
+struct ShardDecision {
+    int max_iters, abort_nonfinite;
+    double rtol, stol;
+    double* hist;     // max_iters + 1 (may be null)
+    double* shist;
+    long long* state;
+};
+
+// carry pass of a fused step (one CTA): [decision of iteration `it`], then the
+// carry z of `rank` from the gathered records, halo += z, and per chunk c:
+// zc[c] = A_cpre[c](z) (zc[nch] is the rank's exit state) and the new state
+// before chunk c's first step: the new halo (c = 0) or bnd[c] + zc[c].
+// Resets the pass's reductions; *stop = 1 skips the rest of the step.
+template <int D>
+__global__ void shard_step_carry_kernel(const double* recs, int rank, int nranks, int it,
+                                        ShardDecision dec, int decide_here, const double* cpre,
+                                        int nch, const double* bnd, double* halo, double* zc,
+                                        double* prevs, unsigned long long* red, int* stop) {
+    constexpr int E = D * D + D, R = ODX_SHARD_REC(D);
+    __shared__ double s_z[4], s_h[4];
+    __shared__ int s_go;
+    if (threadIdx.x == 0) {
+        int go = 1;
+        if (decide_here) {
+            if (it > 0 && dec.state[0]) {
+                go = 0;  // stopped at an earlier iteration
+            } else {
+                constexpr int i_rn = D * D + 2 * D;
+                double rn = 0.0, sc = 0.0, stp = 0.0;
+                unsigned long long bad = ~0ull;
+                for (int q = 0; q < nranks; q++) {
+                    const double* r = recs + (long long)q * R;
+                    rn = nan_drop_max(rn, r[i_rn]);
+                    sc = nan_drop_max(sc, r[i_rn + 1]);
+                    stp = nan_drop_max(stp, r[i_rn + 2]);
+                    const double b = r[i_rn + 3];
+                    if (b >= 0.0 && (unsigned long long)b < bad) bad = (unsigned long long)b;
+                }
+                SolveParams sp;
+                memset(&sp, 0, sizeof(sp));
+                sp.max_iters = dec.max_iters;
+                sp.abort_nonfinite = dec.abort_nonfinite;
+                sp.rtol = dec.rtol;
+                sp.stol = dec.stol;
+                const double step_prev = it > 0 ? stp : __longlong_as_double(0x7ff8000000000000ll);
+                const Decision d = decide(it, sp, rn, bad, step_prev);
+                if (d.status != ODX_ST_SINGULAR) {
+                    if (dec.hist) dec.hist[it] = rn;
+                    if (dec.shist) dec.shist[it] = sc;
+                }
+                if (d.stop) {
+                    dec.state[0] = 1;
+                    dec.state[1] = d.status;
+                    dec.state[2] = d.iters;
+                    dec.state[3] = d.index;
+                    go = 0;
+                } else {
+                    dec.state[0] = 0;
+                }
+            }
+        }
+        s_go = go;
+        *stop = go ? 0 : 1;
+        if (go) {
+            red[0] = red[1] = red[2] = 0ull;
+            red[3] = ~0ull;
+            double v[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q = 0; q < rank; q++) {
+                const double* F = recs + (long long)q * R;
+                double t[4];
+                affine_apply(F, F + D * D, v, D, t);
+                for (int r = 0; r < D; r++) v[r] = t[r];
+            }
+            for (int r = 0; r < D; r++) {
+                s_z[r] = v[r];
+                double h = halo[r];
+                if (rank > 0) {
+                    h = h + v[r];
+                    halo[r] = h;
+                }
+                s_h[r] = h;
+            }
+        }
+    }
+    __syncthreads();
+    if (!s_go) return;
+    for (int c = threadIdx.x; c <= nch; c += blockDim.x) {
+        const double* A = cpre + (long long)c * E;
+        double e[4];
+        affine_apply(A, A + D * D, s_z, D, e);
+        for (int j = 0; j < D; j++) {
+            zc[c * D + j] = e[j];
+            if (c < nch) prevs[c * D + j] = (c == 0) ? s_h[j] : bnd[c * D + j] + e[j];
+        }
+    }
+}
+
 // one row of X: 16-byte stores where the row allows (torch / cudaMalloc rows
 // of d = 2, 4 doubles are 16-byte aligned)
 template <int D>
@@ -541,6 +653,70 @@ int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* h
         tp.cagg, tp.cpre, nch, X_local, n, tp.sp.red, tp.stop, KIND == 0, fused, bnd, per * T, record);
     ODX_CUDA(cudaGetLastError());
     count_launch(fused ? 2 : 3);
+    return ODX_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// One long trajectory on one GPU through the same passes (a "single-rank time
+// shard"): local once, then per iteration [device decision + carry, fused
+// fix-up + build, chunk scan + record], every iteration enqueued up front —
+// passes after the stop decision return at once.  The record of the rank is
+// its own "gathered" record (nranks = 1).
+static __global__ void fused_solve_finish_kernel(const long long* state, int* iters, int* status,
+                                          long long* sidx) {
+    iters[0] = (int)state[2];
+    status[0] = (int)state[1];
+    sidx[0] = state[3];
+}
+
+template <class P, int KIND, int S>
+int fused_tiled_solve(const SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
+                      size_t* need) {
+    constexpr int D = P::D, R = ODX_SHARD_REC(D);
+    constexpr long long T = (long long)SHARD_THREADS * shard_items<D>();
+    const int nch_max = shard_chunks();
+    const ShardTiledLayout<D> lay(p.N, nch_max);
+    const size_t rec_off = align_up(lay.total, 256);
+    const size_t state_off = align_up(rec_off + (size_t)R * 8, 256);
+    const size_t total = state_off + 4 * 8 + 256;
+    if (query) {
+        *need = total;
+        return ODX_OK;
+    }
+    if (!ws || ws_bytes < total) return fail(ODX_EWORKSPACE, "workspace too small");
+    if (reinterpret_cast<uintptr_t>(p.X) & 15) return fail(ODX_EINVAL, "X must be 16-byte aligned");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    double* rec = reinterpret_cast<double*>(base + rec_off);
+    long long* state = reinterpret_cast<long long*>(base + state_off);
+    const long long ntiles = (p.N + T - 1) / T;
+    const int nch = (int)(ntiles < nch_max ? ntiles : nch_max);
+    if (int rc = shard_tiled_local<P, KIND, S>(p.prob, p.sc, p.x0, p.X, p.N, 0, rec, ws, ws_bytes,
+                                               st, 0))
+        return rc;
+    ShardDecision dec;
+    dec.max_iters = p.max_iters;
+    dec.abort_nonfinite = p.abort_nonfinite;
+    dec.rtol = p.rtol;
+    dec.stol = p.stol;
+    dec.hist = p.hist;
+    dec.shist = p.shist;
+    dec.state = state;
+    for (int it = 0; it <= p.max_iters; it++) {
+        shard_step_carry_kernel<D><<<1, 448, 0, st>>>(
+            rec, 0, 1, it, dec, 1, reinterpret_cast<const double*>(base + lay.cpre), nch,
+            reinterpret_cast<const double*>(base + lay.bnd), const_cast<double*>(p.x0),
+            reinterpret_cast<double*>(base + lay.zc), reinterpret_cast<double*>(base + lay.prevs),
+            reinterpret_cast<unsigned long long*>(base + lay.red),
+            reinterpret_cast<int*>(base + lay.stop));
+        count_launch(1);
+        if (int rc = shard_tiled_local<P, KIND, S>(p.prob, p.sc, p.x0, p.X, p.N, 0, rec, ws,
+                                                   ws_bytes, st, 1))
+            return rc;
+    }
+    fused_solve_finish_kernel<<<1, 1, 0, st>>>(state, p.iters, p.status, p.sidx);
+    ODX_CUDA(cudaGetLastError());
+    count_launch(1);
     return ODX_OK;
 }
 

@@ -9,6 +9,7 @@
 #include "dispatch.cuh"
 #include "solve_small.cuh"
 #include "solve_tiled.cuh"
+#include "shard_tiled.cuh"
 #include "solve_ws.cuh"
 
 namespace odx {
@@ -215,6 +216,16 @@ inline bool use_tiled() {
     return on;
 }
 
+// long single trajectories: the fused tiled passes (shard_tiled.cuh) unless
+// ODX_FUSED_TILED=0 selects the streaming warp-specialised kernel
+inline bool use_fused_tiled() {
+    static const bool on = [] {
+        const char* v = std::getenv("ODX_FUSED_TILED");
+        return !(v && std::strcmp(v, "0") == 0);
+    }();
+    return on;
+}
+
 inline bool use_grid_resident() {
     static const bool on = [] {
         const char* v = std::getenv("ODX_GRID_RESIDENT");
@@ -260,6 +271,8 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
             rc = launch_grid_resident<P, KIND, S, 128, GI>(p, ws, ws_bytes, st, query, need);
         if (rc != ODX_EUNSUPPORTED) return rc;
     }
+    if (!resident && p.B == 1 && !small_ws && use_fused_tiled())
+        return fused_tiled_solve<P, KIND, S>(p, ws, ws_bytes, st, query, need);
     if (!resident && p.B == 1 && use_tiled())  // (static smem: T*E*8 <= 48 KB)
         return launch_tiled<P, KIND, S, 128, (D <= 2 ? 4 : 2)>(p, ws, ws_bytes, st, query, need);
     if (query) {

@@ -1,0 +1,78 @@
+"""Every long-trajectory route of the single-GPU solve against the oracle.
+
+The route is chosen once per process from the environment
+(solve_small_launch.cuh), so each case runs in a subprocess:
+  default              fused tiled passes (shard_tiled.cuh: fused_tiled_solve)
+  ODX_FUSED_TILED=0    streaming warp-specialised kernel (solve_ws.cuh)
+  + ODX_TILED=1        two-pass tiled kernels (solve_tiled.cuh)
+"""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+REPO = Path(__file__).resolve().parents[1]
+
+SCRIPT = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2511_01465_b200 as pkg
+from oracle import oracle as O
+name, n, dt, iters = sys.argv[2], int(sys.argv[3]), float(sys.argv[4]), int(sys.argv[5])
+if name == "vdp_rk4":
+    prob, sname = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt), "rk4"
+elif name == "vdp_be":
+    prob, sname = pkg.van_der_pol(mu=10.0, x0=(2.0, 0.0), tf=n * dt), "backward_euler"
+else:
+    prob, sname = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=n * dt), "rk4"
+nat = prob.native()
+pid, params = nat.problem_id, tuple(nat.params[:nat.n_params])
+ost = O.stepper_by_name(sname)
+if sname == "rk4":
+    seq = O.seq_explicit(pid, params, O.RK4_A, O.RK4_B, prob.x0, dt, n)
+else:
+    seq, _ = O.seq_implicit(pid, params, ost.w_prev, ost.w_next, prob.x0, dt, n)
+guess = seq * (1.0 + 1e-3 * np.random.default_rng(3).standard_normal(seq.shape))
+conf = pkg.NewtonConfig(max_iters=iters, abort_on_nonfinite=False)
+rep = pkg.solve(prob, pkg.get_stepper(sname, prob), dt, guess=guess, config=conf)
+ref = O.solve(pid, params, ost, prob.x0, guess, dt, iters, abort_nonfinite=False)
+X = np.asarray(rep.trajectory.states)
+fin = np.isfinite(ref["X"]).all(axis=1)
+scale = max(1.0, float(np.abs(ref["X"][fin]).max()))
+err = float(np.abs(X[fin] - ref["X"][fin]).max()) / scale
+h = np.asarray(rep.residual_history, dtype=float)
+hr = ref["hist"][:len(h)]
+big = hr > 1e-12
+hrel = float(np.max(np.abs(h[big] - hr[big]) / hr[big])) if big.any() else 0.0
+print(json.dumps(dict(err=err, hrel=hrel, iters=rep.iterations_run, ref_iters=ref["iters"],
+                      fin_equal=bool(np.array_equal(fin, np.isfinite(X).all(axis=1))))))
+'''
+
+
+@pytest.mark.parametrize("route", ["fused_tiled", "ws", "tiled"])
+@pytest.mark.parametrize("case", [("vdp_rk4", 1 << 21, 1e-3, 5), ("vdp_be", 600000, 1e-4, 4),
+                                  ("lorenz_rk4", 500001, 1e-5, 4)])
+def test_long_trajectory_routes(case, route):
+    env = dict(os.environ)
+    env.pop("ODX_FUSED_TILED", None)
+    env.pop("ODX_TILED", None)
+    if route != "fused_tiled":
+        env["ODX_FUSED_TILED"] = "0"
+    if route == "tiled":
+        env["ODX_TILED"] = "1"
+    name, n, dt, iters = case
+    out = subprocess.run([sys.executable, "-c", SCRIPT, str(REPO), name, str(n), str(dt),
+                          str(iters)], env=env, capture_output=True, text=True, timeout=600,
+                         cwd=str(REPO))
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["fin_equal"]
+    assert r["err"] <= 1e-9, r
+    assert r["hrel"] <= 1e-7, r
+    assert abs(r["iters"] - r["ref_iters"]) <= 1
