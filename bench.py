@@ -521,6 +521,23 @@ def main():
             except Exception as exc:  # report, never hide
                 extra[f"cfg{ocid}"] = {"error": f"{type(exc).__name__}: {exc}"}
 
+    if not args.no_extra and world > 1 and cid != 5:
+        # cfg5's one trajectory split along time over the N ranks (device-decided
+        # protocol, one NCCL all-gather per iteration): strong scaling against
+        # the N = 1 run's configs["cfg5_..."] entry (same flush, same iterations)
+        try:
+            tw = TimeShardedWorkload(5, args.iters, rank, world)
+            td, tl = time_steps(tw, 3, 2, flush)
+            tms = reduce_max(sum(td), world) / len(td)
+            extra["cfg5_time_sharded"] = {
+                "ranks": world, "fixed_iters": args.iters, "ms": round(tms, 4),
+                "newton_steps_per_s": tw.n_total * args.iters / (tms * 1e-3),
+                "scaling": "strong", "gpu_launches_rank0": tl}
+            del tw
+            torch.cuda.empty_cache()
+        except Exception as exc:  # report, never hide
+            extra["cfg5_time_sharded"] = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(cid, args.iters, args.cpu_seconds)
