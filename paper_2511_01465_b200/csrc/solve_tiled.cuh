@@ -94,30 +94,56 @@ tiled_build_kernel(const TiledParams tp, int it) {
         const long long base = t * T;
         Elem<D> agg;
         bool has = false;
-#pragma unroll
-        for (int q = 0; q < ITEMS; q++) {
-            const long long k = base + (long long)tid * ITEMS + q;
-            if (k < N) {
-                double prev[D], xk[D], h[D];
-#pragma unroll
-                for (int j = 0; j < D; j++) {
-                    prev[j] = (k == 0) ? tp.halo[j] : p.X[(k - 1) * D + j];
-                    xk[j] = p.X[k * D + j];
+        auto take = [&](int q, long long k, const Elem<D>& e, const double* h, bool sing) {
+            rn = nan_drop_max(rn, row_max_abs<D>(h));
+            if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
+            if (sing && (unsigned long long)(tp.offset + k) < bad)
+                bad = (unsigned long long)(tp.offset + k);
+            if (store) {
+                st_elem<D>(&s_el[(tid * ITEMS + q) * E], e);
+                if (has)
+                    compose<D>(agg, e, agg);
+                else {
+                    agg = e;
+                    has = true;
                 }
-                Elem<D> e;
-                const bool sing = build_step<P, KIND, S>(prob, p.sc, prev, xk, tp.offset + k == 0, e, h);
-                rn = nan_drop_max(rn, row_max_abs<D>(h));
-                if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
-                if (sing && (unsigned long long)(tp.offset + k) < bad)
-                    bad = (unsigned long long)(tp.offset + k);
-                if (store) {
-                    st_elem<D>(&s_el[(tid * ITEMS + q) * E], e);
-                    if (has)
-                        compose<D>(agg, e, agg);
-                    else {
-                        agg = e;
-                        has = true;
+            }
+        };
+        const long long kb = base + (long long)tid * ITEMS;
+        if (KIND == 0 && kb + ITEMS <= N) {
+            // explicit, all items present: stage-interleaved build (ILP)
+            double prev[ITEMS][D], xk[ITEMS][D], h[ITEMS][D];
+            bool first[ITEMS];
+            Elem<D> e[ITEMS];
+#pragma unroll
+            for (int j = 0; j < D; j++) prev[0][j] = (kb == 0) ? tp.halo[j] : p.X[(kb - 1) * D + j];
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) {
+#pragma unroll
+                for (int j = 0; j < D; j++) xk[q][j] = p.X[(kb + q) * D + j];
+                if (q + 1 < ITEMS)
+#pragma unroll
+                    for (int j = 0; j < D; j++) prev[q + 1][j] = xk[q][j];
+                first[q] = (tp.offset + kb + q == 0);
+            }
+            build_explicit_multi<P, S, ITEMS>(prob, p.sc, prev, xk, first, e, h);
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) take(q, kb + q, e[q], h[q], false);
+        } else {
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) {
+                const long long k = kb + q;
+                if (k < N) {
+                    double prev[D], xk[D], h[D];
+#pragma unroll
+                    for (int j = 0; j < D; j++) {
+                        prev[j] = (k == 0) ? tp.halo[j] : p.X[(k - 1) * D + j];
+                        xk[j] = p.X[k * D + j];
                     }
+                    Elem<D> e;
+                    const bool sing =
+                        build_step<P, KIND, S>(prob, p.sc, prev, xk, tp.offset + k == 0, e, h);
+                    take(q, k, e, h, sing);
                 }
             }
         }
@@ -128,15 +154,13 @@ tiled_build_kernel(const TiledParams tp, int it) {
             st_elem<D>(s_wt[w], agg);
             s_wh[w] = has ? 1 : 0;
         }
+        fence_proxy_async_smem();  // staged elements -> the bulk store (async proxy)
         __syncthreads();
-        // coalesced write-out of the tile's elements
+        // the tile's elements: one bulk copy (rows*E*8 is a multiple of 16)
         const long long rows = (N - base) < T ? (N - base) : T;
-        {
-            const int nd = (int)(rows * E);
-            double* dst = tp.el + base * E;
-            for (int q = tid; q < nd; q += THREADS) dst[q] = s_el[q];
-        }
         if (tid == 0) {
+            tma_store_1d(tp.el + base * E, s_el, (uint32_t)(rows * E * 8));
+            tma_store_commit();
             for (int q = 0; q < NW; q++) {
                 if (!s_wh[q]) continue;
                 Elem<D> a;
@@ -148,10 +172,12 @@ tiled_build_kernel(const TiledParams tp, int it) {
                     chunk_has = true;
                 }
             }
+            tma_store_wait_read();  // s_el is rewritten after the sync below
         }
         __syncthreads();
     }
     if (store && tid == 0) {
+        tma_store_wait_all();
         if (!chunk_has) set_identity<D>(chunk);
         st_elem<D>(tp.cagg + (long long)blockIdx.x * E, chunk);
     }
