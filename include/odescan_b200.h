@@ -251,6 +251,30 @@ int odx_shard_decide_step(const odx_problem* P, const odx_stepper* S,
                           double* hist, double* scaled_hist, int64_t* state,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- the whole time-sharded solve natively (SURVEY §8b odx_solve_sharded) ----
+ * One call per rank runs odx_shard_local, then per iteration it = 0..max_iters
+ * ncclAllGather(record -> records) + odx_shard_decide_step, everything on
+ * `stream` (no host round trip).  comm is an ncclComm_t of the process's
+ * libnccl.so.2 (odx_nccl_comm_init makes one; a communicator created by the
+ * caller with the same library works too).  halo: device, d doubles (x0 on rank
+ * 0, else rank r-1's last guess row; not modified).  state: device int64[4]
+ * {stopped, status, iterations, status_index}; hist / scaled_hist: device,
+ * max_iters + 1 (entries past the stop untouched; may be NULL).  poll > 0:
+ * read the stop flag every `poll` iterations (a stream sync) and stop
+ * enqueuing once stopped — identical on every rank; poll = 0: fully
+ * asynchronous (iterations after the stop are no-ops).                        */
+int    odx_nccl_available(void);
+int    odx_nccl_unique_id(void* id /* 128 bytes */);
+int    odx_nccl_comm_init(void** comm, int32_t nranks, const void* id, int32_t rank);
+int    odx_nccl_comm_destroy(void* comm);
+size_t odx_solve_sharded_workspace_bytes(const odx_problem* P, const odx_stepper* S,
+                                         int64_t N_local, int32_t nranks);
+int    odx_solve_sharded(const odx_problem* P, const odx_stepper* S, const odx_newton_cfg* C,
+                         void* comm, int32_t rank, int32_t nranks, const double* halo,
+                         double* X_local, int64_t N_local, int64_t offset, double dt,
+                         double* hist, double* scaled_hist, int64_t* state, int32_t poll,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,8 @@ EXPORTS = (
     "odx_solve", "odx_solve_host", "odx_initial_guess", "odx_seq_march", "odx_parareal_coarse", "odx_build_explicit", "odx_build_implicit",
     "odx_scan_affine_workspace_bytes", "odx_scan_affine", "odx_max_abs", "odx_add_inplace",
     "odx_shard_workspace_bytes", "odx_shard_local", "odx_shard_fixup", "odx_shard_step",
-    "odx_shard_decide_step",
+    "odx_shard_decide_step", "odx_nccl_available", "odx_nccl_unique_id", "odx_nccl_comm_init",
+    "odx_nccl_comm_destroy", "odx_solve_sharded_workspace_bytes", "odx_solve_sharded",
 )
 
 
@@ -109,6 +110,19 @@ def lib():
     L.odx_shard_fixup.argtypes = [P_, vp, i32, i32, vp, i64, vp, vp, vp, sz, vp]
     L.odx_shard_step.restype = C.c_int
     L.odx_shard_step.argtypes = [P_, S_, vp, i32, i32, vp, vp, i64, i64, dbl, vp, vp, sz, vp]
+    L.odx_nccl_available.restype = C.c_int
+    L.odx_nccl_available.argtypes = []
+    L.odx_nccl_unique_id.restype = C.c_int
+    L.odx_nccl_unique_id.argtypes = [vp]
+    L.odx_nccl_comm_init.restype = C.c_int
+    L.odx_nccl_comm_init.argtypes = [C.POINTER(C.c_void_p), i32, vp, i32]
+    L.odx_nccl_comm_destroy.restype = C.c_int
+    L.odx_nccl_comm_destroy.argtypes = [vp]
+    L.odx_solve_sharded_workspace_bytes.restype = sz
+    L.odx_solve_sharded_workspace_bytes.argtypes = [P_, S_, i64, i32]
+    L.odx_solve_sharded.restype = C.c_int
+    L.odx_solve_sharded.argtypes = [P_, S_, CFG, vp, i32, i32, vp, vp, i64, i64, dbl, vp, vp, vp,
+                                    i32, vp, sz, vp]
     L.odx_shard_decide_step.restype = C.c_int
     L.odx_shard_decide_step.argtypes = [P_, S_, CFG, vp, i32, i32, i32, vp, vp,
                                         i64, i64, dbl, vp, vp, vp, vp, vp, sz, vp]

@@ -13,6 +13,7 @@
 // are shared).
 #include <pthread.h>
 
+#include <algorithm>
 #include <atomic>
 #include <emmintrin.h>
 #include <chrono>
@@ -76,9 +77,11 @@ int grow_pinned(void** p, size_t* have, size_t need) {
 inline size_t al256(size_t v) { return (v + 255) & ~size_t(255); }
 
 // Host memcpy of the staging path split over a small persistent worker pool
-// (one core copies ~20 GB/s; the trajectory is MBs).  Workers sleep on a
-// condition variable between calls; ODX_HOST_THREADS sets the pool size
-// (default 4, 0 or 1 = plain memcpy).
+// (one core copies ~15-20 GB/s; the trajectory is MBs).  After a job the
+// workers spin for a short while (back-to-back solves find them awake, no
+// futex wake-up on the critical path), then sleep on a condition variable.
+// ODX_HOST_THREADS sets the pool size (default: 8, at most half the cores;
+// 0 or 1 = plain memcpy).
 // Copy with non-temporal stores: the destination (pinned staging the DMA
 // engine reads next, or the caller's result) does not linger dirty in this
 // core's caches, so the device's reads of it need no cross-core snoops.
@@ -110,56 +113,62 @@ class CopyPool {
     void copy(void* dst, const void* src, size_t n) {
         // a forked child has no worker threads (fork copies only the caller)
         const int T = forked_.load(std::memory_order_relaxed) ? 0 : (int)workers_.size();
-        if (T == 0 || n < (size_t(1) << 19)) {
+        if (T == 0 || n < (size_t(1) << 18)) {
             nt_copy(static_cast<char*>(dst), static_cast<const char*>(src), n);
             return;
         }
         const int parts = T + 1;
         const size_t chunk = ((n + parts - 1) / parts + 63) & ~size_t(63);
-        {
+        dst_ = static_cast<char*>(dst);
+        src_ = static_cast<const char*>(src);
+        n_ = n;
+        chunk_ = chunk;
+        pending_.store(T, std::memory_order_relaxed);
+        gen_.fetch_add(1, std::memory_order_seq_cst);  // publishes the job (release)
+        if (sleepers_.load(std::memory_order_seq_cst) > 0) {
             std::lock_guard<std::mutex> lk(mu_);
-            dst_ = static_cast<char*>(dst);
-            src_ = static_cast<const char*>(src);
-            n_ = n;
-            chunk_ = chunk;
-            pending_.store(T, std::memory_order_relaxed);
-            gen_++;
+            cv_.notify_all();
         }
-        cv_.notify_all();
         const size_t lo = (size_t)T * chunk;  // the caller copies the last part
         if (lo < n) nt_copy(dst_ + lo, src_ + lo, n - lo);
-        while (pending_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+        while (pending_.load(std::memory_order_acquire) != 0) _mm_pause();
     }
 
   private:
     CopyPool() {
         pthread_atfork(nullptr, nullptr, [] { get().forked_.store(true); });
         const char* e = std::getenv("ODX_HOST_THREADS");
-        int t = e ? std::atoi(e) : 4;
+        const int hw = (int)std::thread::hardware_concurrency();
+        int t = e ? std::atoi(e) : std::min(8, std::max(1, hw / 2));
         if (t > 1)
             for (int i = 0; i < t - 1; i++) workers_.emplace_back([this, i] { run(i); });
     }
     void run(int i) {
         unsigned long long seen = 0;
         while (true) {
-            char* d;
-            const char* s;
-            size_t n, chunk;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
-                d = dst_, s = src_, n = n_, chunk = chunk_;
+            // spin ~0.5 ms for the next job, then sleep
+            bool got = false;
+            for (int k = 0; k < 20000 && !got; k++) {
+                if (gen_.load(std::memory_order_acquire) != seen) got = true;
+                else _mm_pause();
             }
-            const size_t lo = (size_t)i * chunk;
-            if (lo < n) nt_copy(d + lo, s + lo, (lo + chunk < n ? chunk : n - lo));
+            if (!got) {
+                std::unique_lock<std::mutex> lk(mu_);
+                sleepers_.fetch_add(1, std::memory_order_seq_cst);
+                cv_.wait(lk, [&] { return gen_.load(std::memory_order_seq_cst) != seen; });
+                sleepers_.fetch_sub(1, std::memory_order_relaxed);
+            }
+            seen = gen_.load(std::memory_order_acquire);
+            const size_t lo = (size_t)i * chunk_;
+            if (lo < n_) nt_copy(dst_ + lo, src_ + lo, (lo + chunk_ < n_ ? chunk_ : n_ - lo));
             pending_.fetch_sub(1, std::memory_order_release);
         }
     }
     std::vector<std::thread> workers_;
     std::mutex mu_;
     std::condition_variable cv_;
-    unsigned long long gen_ = 0;
+    std::atomic<unsigned long long> gen_{0};
+    std::atomic<int> sleepers_{0};
     char* dst_ = nullptr;
     const char* src_ = nullptr;
     size_t n_ = 0, chunk_ = 0;

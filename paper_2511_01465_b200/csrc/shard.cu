@@ -13,10 +13,18 @@
 //                     max|dx| -> step; the last row is set to x_last + A_r(z_r)
 //                     and halo += z_r, both from the same affine map, so the
 //                     halo is bit-identical to rank r-1's new last row.
+//   odx_solve_sharded: the whole loop on one rank natively — local, then per
+//                     iteration ncclAllGather of the records + the
+//                     device-decided step, all on the caller's stream (NCCL
+//                     is resolved at run time from the process's libnccl.so.2,
+//                     the one torch loaded when present).
 //   odx_shard_step  : fixup + the next iteration's local in one pass over the
 //                     rank's steps (shard_tiled.cuh: shard_fused_kernel); the
 //                     carry pass below precomputes every chunk's incoming
 //                     update state with the same affine map.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <climits>
 #include <cstring>
 
@@ -222,6 +230,149 @@ int odx_shard_fixup(const odx_problem* P, const double* records, int32_t rank, i
         return shard_fixup_d<D>(records, rank, X_local, N_local, halo, step_out, workspace,
                                 workspace_bytes, (cudaStream_t)stream);
     });
+}
+
+
+}  // extern "C"
+
+namespace odx {
+namespace {
+// NCCL entry points resolved at run time: the library torch already loaded
+// (so communicators made by either side are the same library's), else the
+// system libnccl.so.2.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_gather;
+        return a;
+    }();
+    return api;
+}
+int nccl_fail(ncclResult_t r, const char* what) {
+    const NcclApi& a = nccl_api();
+    std::string m = std::string(what) + ": " + (a.error_string ? a.error_string(r) : "NCCL error");
+    return fail(ODX_ECUDA, m.c_str());
+}
+size_t al256s(size_t v) { return (v + 255) & ~size_t(255); }
+}  // namespace
+}  // namespace odx
+
+extern "C" {
+
+int odx_nccl_available(void) { return odx::nccl_api().ok ? 1 : 0; }
+
+int odx_nccl_unique_id(void* id) {
+    using namespace odx;
+    if (!id) return fail(ODX_EINVAL, "null id buffer");
+    if (!nccl_api().ok) return fail(ODX_EUNSUPPORTED, "libnccl.so.2 not found");
+    ncclUniqueId u;
+    if (ncclResult_t r = nccl_api().get_unique_id(&u)) return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+    return ODX_OK;
+}
+
+int odx_nccl_comm_init(void** comm, int32_t nranks, const void* id, int32_t rank) {
+    using namespace odx;
+    if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(ODX_EINVAL, "bad communicator arguments");
+    if (!nccl_api().ok) return fail(ODX_EUNSUPPORTED, "libnccl.so.2 not found");
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    ncclComm_t c = nullptr;
+    if (ncclResult_t r = nccl_api().comm_init_rank(&c, nranks, u, rank))
+        return nccl_fail(r, "ncclCommInitRank");
+    *comm = c;
+    return ODX_OK;
+}
+
+int odx_nccl_comm_destroy(void* comm) {
+    using namespace odx;
+    if (!comm) return ODX_OK;
+    if (!nccl_api().ok) return fail(ODX_EUNSUPPORTED, "libnccl.so.2 not found");
+    if (ncclResult_t r = nccl_api().comm_destroy(static_cast<ncclComm_t>(comm)))
+        return nccl_fail(r, "ncclCommDestroy");
+    return ODX_OK;
+}
+
+size_t odx_solve_sharded_workspace_bytes(const odx_problem* P, const odx_stepper* S,
+                                         int64_t N_local, int32_t nranks) {
+    const size_t sh = odx_shard_workspace_bytes(P, S, N_local);
+    if (sh == 0 || nranks < 1) return 0;
+    const int R = ODX_SHARD_REC(P->dim);
+    return odx::al256s(sh) + odx::al256s((size_t)R * 8) + odx::al256s((size_t)nranks * R * 8) +
+           odx::al256s((size_t)P->dim * 8) + 256;
+}
+
+int odx_solve_sharded(const odx_problem* P, const odx_stepper* S, const odx_newton_cfg* C,
+                      void* comm, int32_t rank, int32_t nranks, const double* halo,
+                      double* X_local, int64_t N_local, int64_t offset, double dt, double* hist,
+                      double* scaled_hist, int64_t* state, int32_t poll, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+    using namespace odx;
+    if (!P || !S || P->dim < 1 || P->dim > 4 || dense_supported(P, S))
+        return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
+    if (!C || C->max_iters < 1) return fail(ODX_EINVAL, "max_iters must be >= 1");
+    if (!comm) return fail(ODX_EINVAL, "null NCCL communicator");
+    if (rank < 0 || rank >= nranks || N_local < 1 || offset < 0)
+        return fail(ODX_EINVAL, "bad rank / extent");
+    if (!halo || !X_local || !state) return fail(ODX_EINVAL, "null device buffer");
+    if (!nccl_api().ok) return fail(ODX_EUNSUPPORTED, "libnccl.so.2 not found");
+    const size_t need = odx_solve_sharded_workspace_bytes(P, S, N_local, nranks);
+    if (!workspace || workspace_bytes < need) return fail(ODX_EWORKSPACE, "sharded workspace");
+    const int d = P->dim, R = ODX_SHARD_REC(d);
+    const size_t sh = odx_shard_workspace_bytes(P, S, N_local);
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(workspace), 256));
+    char* w2 = base + al256s(sh);
+    double* rec = reinterpret_cast<double*>(w2);
+    double* recs = reinterpret_cast<double*>(w2 + al256s((size_t)R * 8));
+    double* halo_w = reinterpret_cast<double*>(w2 + al256s((size_t)R * 8) +
+                                               al256s((size_t)nranks * R * 8));
+    cudaStream_t st = (cudaStream_t)stream;
+    ncclComm_t cm = static_cast<ncclComm_t>(comm);
+    ODX_CUDA(cudaMemcpyAsync(halo_w, halo, (size_t)d * 8, cudaMemcpyDeviceToDevice, st));
+    if (int rc = odx_shard_local(P, S, halo_w, X_local, N_local, offset, dt, rec, base, sh, stream))
+        return rc;
+    ShardDecision dec;
+    dec.max_iters = C->max_iters;
+    dec.abort_nonfinite = C->abort_nonfinite;
+    dec.rtol = C->residual_tol;
+    dec.stol = C->step_tol;
+    dec.hist = hist;
+    dec.shist = scaled_hist;
+    dec.state = reinterpret_cast<long long*>(state);
+    for (int it = 0; it <= C->max_iters; it++) {
+        if (ncclResult_t r = nccl_api().all_gather(rec, recs, (size_t)R, ncclDouble, cm, st))
+            return nccl_fail(r, "ncclAllGather");
+        const int rc = with_dim(d, [&]<int D>() {
+            return shard_step_d<D>(P, S, recs, rank, nranks, it, &dec, halo_w, X_local, N_local,
+                                   offset, dt, rec, base, sh, st);
+        });
+        if (rc) return rc;
+        if (poll > 0 && it < C->max_iters && (it + 1) % poll == 0) {
+            long long stopped = 0;  // identical on every rank: all leave together
+            ODX_CUDA(cudaMemcpyAsync(&stopped, state, 8, cudaMemcpyDeviceToHost, st));
+            ODX_CUDA(cudaStreamSynchronize(st));
+            if (stopped) break;
+        }
+    }
+    return ODX_OK;
 }
 
 }  // extern "C"

@@ -341,11 +341,17 @@ def _solve_host(P, S, x0s: np.ndarray, X: np.ndarray, dt: float, config: NewtonC
     sidx = np.empty(B, dtype=np.int64)
     cfg = N.make_cfg(config.max_iters, config.residual_tol, config.step_tol,
                      config.abort_on_nonfinite)
-    with torch.cuda.device(dev):
+
+    def call():
         N.check(N.lib().odx_solve_host(
             P, S, x0c.ctypes.data, Xc.ctypes.data, states.ctypes.data, B, n, float(dt), cfg,
             hist.ctypes.data, shist.ctypes.data, iters.ctypes.data, status.ctypes.data,
             sidx.ctypes.data, torch.cuda.current_stream(dev).cuda_stream))
+    if dev.index == torch.cuda.current_device():
+        call()  # (the device switch costs ~6 us per call)
+    else:
+        with torch.cuda.device(dev):
+            call()
     return states, hist, shist, iters, status, sidx
 
 

@@ -229,13 +229,73 @@ def run_device_decided(shards, gather_into, config, poll: int = 8) -> dict:
             s.decide_step(it, cfg, h, sh, st)
         if it < m and (it + 1) % poll == 0 and int(bufs[0][2][0].item()):
             break
-    h, sh, st = (b.cpu().numpy() for b in bufs[0])
+    return _decided_outcome(*bufs[0])
+
+
+def _decided_outcome(hist, shist, state) -> dict:
+    """ShardedNewton.run()'s dict from the device-side decision buffers."""
+    h, sh, st = (b.cpu().numpy() for b in (hist, shist, state))
     stopped, status, iters, idx = (int(v) for v in st)
     if not stopped:
         raise RuntimeError("device-decided protocol did not reach a decision")
     n_hist = iters + 1 - (1 if status == N.ST_SINGULAR else 0)
     return dict(hist=[float(v) for v in h[:n_hist]], shist=[float(v) for v in sh[:n_hist]],
                 iters=iters, status=status, status_index=idx)
+
+
+_COMMS: dict = {}
+
+
+def nccl_comm(group=None) -> int:
+    """An ncclComm_t of this process's libnccl.so.2 over the ranks of `group`
+    (made once per group and device; rank 0's unique id is broadcast through
+    torch.distributed).  Used by the native loop, odx_solve_sharded."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    key = (id(group), torch.cuda.current_device())
+    if key in _COMMS:
+        return _COMMS[key]
+    L = N.lib()
+    if not L.odx_nccl_available():
+        raise RuntimeError("libnccl.so.2 is not loadable: use protocol='device'")
+    R, r = dist.get_world_size(group), dist.get_rank(group)
+    uid = C.create_string_buffer(128)
+    if r == 0:
+        N.check(L.odx_nccl_unique_id(uid))
+    obj = [uid.raw]
+    src = 0 if group is None else dist.get_global_rank(group, 0)
+    dist.broadcast_object_list(obj, src=src, group=group)
+    uid = C.create_string_buffer(obj[0], 128)
+    comm = C.c_void_p()
+    N.check(L.odx_nccl_comm_init(C.byref(comm), R, uid, r))
+    _COMMS[key] = comm.value
+    return comm.value
+
+
+def run_native(problem, stepper, dt, X_local, halo, offset, rank, nranks, comm, config,
+               poll: int = 8) -> dict:
+    """The whole per-rank loop in one library call (odx_solve_sharded): local
+    pass, then per iteration ncclAllGather + device-decided fused step, all on
+    the current stream."""
+    import torch
+    L = N.lib()
+    P, S = problem.native(), stepper.native()
+    dev = X_local.device
+    n = X_local.shape[0]
+    m = int(config.max_iters)
+    cfg = N.make_cfg(m, config.residual_tol, config.step_tol, config.abort_on_nonfinite)
+    wsb = L.odx_solve_sharded_workspace_bytes(P, S, n, nranks)
+    if wsb == 0:
+        raise ValueError("time sharding supports small state dims (d <= 4)")
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    hist = torch.full((m + 1,), math.nan, dtype=torch.float64, device=dev)
+    shist = torch.full((m + 1,), math.nan, dtype=torch.float64, device=dev)
+    state = torch.zeros(4, dtype=torch.int64, device=dev)
+    N.check(L.odx_solve_sharded(P, S, cfg, comm, rank, nranks, N.ptr(halo), N.ptr(X_local), n,
+                                int(offset), float(dt), N.ptr(hist), N.ptr(shist), N.ptr(state),
+                                int(poll), N.ptr(ws), wsb, N.stream_handle(dev)))
+    return _decided_outcome(hist, shist, state)
 
 
 def _torch_gather(group, d, device):
@@ -259,8 +319,11 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
     """Time-sharded solve of one trajectory across the ranks of `group`.
 
     protocol: "device" (default) — fused passes, decision on the device, no
-    host round trip per iteration; "host" — fused passes, decision on the
-    host (ShardedNewton); "two_pass" — separate local / fix-up passes.
+    host round trip per iteration, the loop and torch's NCCL all-gather
+    driven from Python; "native" — the same loop inside the library
+    (odx_solve_sharded, its own NCCL communicator); "host" — fused passes,
+    decision on the host (ShardedNewton); "two_pass" — separate local /
+    fix-up passes.
 
     X_local: this rank's (n_local, d) CUDA tensor of the initial guess (updated
     in place to the final iterate).  Chunks must be contiguous and ordered by
@@ -269,7 +332,7 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
     """
     import torch
     import torch.distributed as dist
-    if protocol not in ("device", "host", "two_pass"):
+    if protocol not in ("device", "native", "host", "two_pass"):
         raise ValueError(f"unknown protocol {protocol!r}")
     R = dist.get_world_size(group)
     r = dist.get_rank(group)
@@ -281,7 +344,10 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
     dist.all_gather_into_tensor(lasts, last, group=group)
     x0 = torch.as_tensor(problem.x0, dtype=torch.float64, device=dev)
     halo = x0 if r == 0 else lasts[r - 1].clone()
-    if protocol == "device":
+    if protocol == "native":
+        out = run_native(problem, stepper, dt, X_local, halo.contiguous(), offset, r, R,
+                         nccl_comm(group), config)
+    elif protocol == "device":
         shard = DeviceShard(problem, stepper, dt, X_local, halo, offset, r, R, fused=True)
 
         def gather_into():

@@ -109,17 +109,25 @@ def test_nccl_drivers_world_size_one(oracle):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        n, dt = 8192, 1e-3
+        n, dt = 200000, 1e-3
         prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
         st = pkg.get_stepper("rk4", prob)
-        X = torch.from_numpy(np.tile(prob.x0, (n, 1))).cuda()
-        conf = pkg.NewtonConfig(max_iters=4, abort_on_nonfinite=False)
-        rep = solve_time_sharded(prob, st, dt, X, 0, conf)
-        ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), prob.x0,
-                           np.tile(prob.x0, (n, 1)), dt, 4, abort_nonfinite=False)
-        assert rep.iterations_run == 4
+        seq = oracle.seq_explicit(1, (1.0,), oracle.RK4_A, oracle.RK4_B, prob.x0, dt, n)
+        guess = seq * (1.0 + 1e-3 * np.random.default_rng(5).standard_normal(seq.shape))
+        ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), prob.x0, guess, dt, 12,
+                           step_tol=1e-10, abort_nonfinite=False)
+        assert ref["status"] == oracle.ST_CONVERGED and ref["iters"] < 12
         scale = max(1.0, float(np.abs(ref["X"]).max()))
-        assert np.abs(X.cpu().numpy() - ref["X"]).max() <= 1e-9 * scale
+        for protocol in ("native", "device", "host", "two_pass"):
+            X = torch.from_numpy(guess.copy()).cuda()
+            conf = pkg.NewtonConfig(max_iters=12, step_tol=1e-10, abort_on_nonfinite=False)
+            rep = solve_time_sharded(prob, st, dt, X, 0, conf, protocol=protocol)
+            assert rep.status == ref["status"], protocol
+            assert abs(rep.iterations_run - ref["iters"]) <= 1, protocol
+            assert np.abs(X.cpu().numpy() - ref["X"]).max() <= 1e-9 * scale, protocol
+            h = np.array(rep.residual_history)
+            hr = ref["hist"][:len(h)]
+            assert (np.abs(h - hr) <= 1e-7 * hr + 1e-9 * hr[0]).all(), protocol
         cfg = CONFIGS[3]
         lor = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=cfg.n_steps * cfg.dt)
         local, off, gathered = solve_batch_sharded(lor, pkg.get_stepper("rk4", lor), cfg.dt,
