@@ -392,6 +392,16 @@ def _fetch(dev_tensor, key):
     return dst
 
 
+def _fetch_owned(dev_tensor):
+    """Device -> a fresh page-locked host tensor (PyTorch's caching host
+    allocator, so no per-call cudaHostAlloc); the numpy view returned after the
+    sync keeps it alive, so no host-side copy is needed."""
+    import torch
+    dst = torch.empty(dev_tensor.shape, dtype=dev_tensor.dtype, pin_memory=True)
+    dst.copy_(dev_tensor, non_blocking=True)
+    return dst
+
+
 def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones",
           config: NewtonConfig | None = None, *, device=None, output: str = "numpy"
           ) -> SolveReport:
@@ -430,10 +440,10 @@ def solve(problem: OdeProblem, stepper: StepperIncrement, dt: float, guess="ones
     H = config.max_iters + 1
     out = solve_device(P, S, x0, X, dt, config)
     out_h = _fetch(out, ("out", dev))
-    states_h = None if output == "torch" else _fetch(X[0], ("Xo", dev))
+    states_h = None if output == "torch" else _fetch_owned(X[0])
     torch.cuda.current_stream(dev).synchronize()
     hist, shist, iters, status, sidx = _unpack_outcome(out_h.numpy(), 1, H)
-    states = X[0] if output == "torch" else states_h.numpy().copy()
+    states = X[0] if output == "torch" else states_h.numpy()
     return _report(problem, config, dt, n, states, hist, shist, iters, status, sidx, t_begin)
 
 
@@ -507,11 +517,11 @@ def solve_batch(problem: OdeProblem, stepper: StepperIncrement, dt: float, x0s, 
     H = config.max_iters + 1
     out = solve_device(P, S, x0t, X, dt, config)
     out_h = _fetch(out, ("out", dev))
-    states_h = None if output == "torch" else _fetch(X, ("Xo", dev))
+    states_h = None if output == "torch" else _fetch_owned(X)
     torch.cuda.current_stream(dev).synchronize()
     hist, shist, iters, status, sidx = _unpack_outcome(out_h.numpy(), B, H)
     rep = BatchSolveReport(
-        states=X if output == "torch" else states_h.numpy().copy(),
+        states=X if output == "torch" else states_h.numpy(),
         residual_history=hist, scaled_residual_history=shist, iterations_run=iters,
         status=status, status_index=sidx, wall_time=0.0)
     rep.wall_time = time.perf_counter() - t_begin
