@@ -379,13 +379,15 @@ __device__ __forceinline__ void gemm64_store(double* C, const double (&acc)[8][2
     }
 }
 
-// y_out = M y + v (M row-major ld FLD in smem, y/v in smem); 4 threads per row
+// y_out = M y + v (M row-major ld FLD in smem, y/v in smem); 4 threads per
+// row, thread `part` taking columns part, part+4, ... so a half-warp's 16
+// loads (4 rows x 4 parts) fall on 16 distinct bank pairs
 __device__ __forceinline__ void matvec64(const double* M, const double* y, const double* v,
                                          double* out) {
     const int tid = threadIdx.x, r = tid >> 2, part = tid & 3;
     double acc = 0.0;
 #pragma unroll
-    for (int q = 0; q < 16; q++) acc += M[r * FLD + part * 16 + q] * y[part * 16 + q];
+    for (int q = 0; q < 16; q++) acc += M[r * FLD + part + 4 * q] * y[part + 4 * q];
     acc += __shfl_xor_sync(FULL, acc, 1);
     acc += __shfl_xor_sync(FULL, acc, 2);
     if (part == 0) out[r] = acc + v[r];
@@ -465,11 +467,13 @@ __global__ void __launch_bounds__(DTHREADS) dense_agg_kernel(const DenseParams p
 // =========================================================================
 // K3: incoming states of the chunks  z_{c+1} = P_c z_c + y_c  (one CTA)
 // =========================================================================
+constexpr int FOLD_BUF = 5;  // aggregates in flight: the chain is bound by one SM's load rate
+
 struct FoldSmem {
-    double Ab[2][DN * FLD];
-    double ab[2][DN];
+    double Ab[FOLD_BUF][DN * FLD];
+    double ab[FOLD_BUF][DN];
     double z[2][DN];
-    uint64_t bar[2];
+    uint64_t bar[FOLD_BUF];
 };
 
 __global__ void __launch_bounds__(DTHREADS) dense_fold_kernel(const DenseParams p) {
@@ -479,8 +483,7 @@ __global__ void __launch_bounds__(DTHREADS) dense_fold_kernel(const DenseParams 
     const int tid = threadIdx.x;
     const int C = p.nchunks;
     if (tid == 0) {
-        mbar_init(&sm.bar[0], 1);
-        mbar_init(&sm.bar[1], 1);
+        for (int b = 0; b < FOLD_BUF; b++) mbar_init(&sm.bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < DN) {
@@ -497,17 +500,14 @@ __global__ void __launch_bounds__(DTHREADS) dense_fold_kernel(const DenseParams 
         }
     };
     if (tid == 0) fence_proxy_async_global();
-    if (C > 1) stage_agg(0, 0);
-    if (C > 2) stage_agg(1, 1);
-    uint32_t ph[2] = {0, 0};
+    for (int q = 0; q < FOLD_BUF && q + 1 < C; q++) stage_agg(q, q);
     int zb = 0;
     for (int q = 0; q + 1 < C; q++) {
-        const int b = q & 1;
-        mbar_wait(&sm.bar[b], ph[b]);
-        ph[b] ^= 1;
+        const int b = q % FOLD_BUF;
+        mbar_wait(&sm.bar[b], (uint32_t)((q / FOLD_BUF) & 1));  // k-th use of buffer b
         matvec64(sm.Ab[b], sm.z[zb], sm.ab[b], sm.z[zb ^ 1]);
         __syncthreads();
-        if (q + 3 < C) stage_agg(q + 2, b);
+        if (q + FOLD_BUF + 1 < C) stage_agg(q + FOLD_BUF, b);
         zb ^= 1;
         if (tid < DN) p.zin[(long long)(q + 1) * DN + tid] = sm.z[zb][tid];
     }
