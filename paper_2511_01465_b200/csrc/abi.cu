@@ -44,6 +44,9 @@ int add_op(double* X, const double* U, long long n, int d, cudaStream_t st);
 
 // d = 64 dense path (solve_dense.cu)
 int dense_supported(const odx_problem* P, const odx_stepper* S);
+int dense_shard_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
+                      const double* X_local, long long n, long long offset, double* record,
+                      void* ws, size_t ws_bytes, cudaStream_t st);
 int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
                 size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
 int dense_build_op(const odx_problem* P, const odx_stepper* S, const StepCoefs& sc,
@@ -309,6 +312,10 @@ int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
     StepCoefs sc;
     if (!fill_params(P, pp)) return fail(ODX_EINVAL, "bad problem parameters");
     if (!fill_coefs(S, dt, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
+    if (dense_supported(P, S)) {
+        if (fused) return fail(ODX_EUNSUPPORTED, "the d = 64 shard runs the two-pass protocol");
+        return dense_shard_local(pp, sc, halo, X_local, n, offset, record, ws, ws_bytes, st);
+    }
     ShardLocalFn fn{S, &pp, &sc, halo, X_local, n, offset, record, ws, ws_bytes, st, fused};
     return with_small_problem(P->problem_id, P->dim, fn);
 }

@@ -37,6 +37,12 @@ int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
                          const double* halo, const double* X_local, long long n, long long offset,
                          double* record, void* ws, size_t ws_bytes, cudaStream_t st, int fused);
 int dense_supported(const odx_problem* P, const odx_stepper* S);
+size_t dense_shard_workspace(long long n);
+int dense_shard_fixup(const double* records, int rank, double* X_local, long long n, double* halo,
+                      double* step_out, void* ws, size_t ws_bytes, cudaStream_t st);
+inline bool dense_problem(const odx_problem* P) {
+    return P && P->problem_id == ODX_PROB_ALLEN_CAHN && P->dim == 64;
+}
 
 // carry z of `rank` and its exit state dlast = A_rank(z); halo += z (rank > 0);
 // the step slot of the reduction quad is reset
@@ -157,6 +163,7 @@ using namespace odx;
 extern "C" {
 
 size_t odx_shard_workspace_bytes(const odx_problem* P, const odx_stepper* S, int64_t N_local) {
+    if (P && S && N_local >= 1 && dense_supported(P, S)) return dense_shard_workspace(N_local);
     if (!P || !S || P->dim < 1 || P->dim > 4 || N_local < 1 || dense_supported(P, S)) return 0;
     size_t total = 0;
     with_dim(P->dim, [&]<int D>() {
@@ -169,8 +176,8 @@ size_t odx_shard_workspace_bytes(const odx_problem* P, const odx_stepper* S, int
 int odx_shard_local(const odx_problem* P, const odx_stepper* S, const double* halo,
                     const double* X_local, int64_t N_local, int64_t offset, double dt,
                     double* record, void* workspace, size_t workspace_bytes, void* stream) {
-    if (!P || !S || P->dim < 1 || P->dim > 4 || dense_supported(P, S))
-        return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
+    if (!P || !S || ((P->dim < 1 || P->dim > 4) && !dense_supported(P, S)))
+        return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4 and the d = 64 Allen-Cahn path");
     if (N_local < 1 || offset < 0) return fail(ODX_EINVAL, "bad shard extent");
     if (!halo || !X_local || !record) return fail(ODX_EINVAL, "null device buffer");
     if (reinterpret_cast<uintptr_t>(X_local) & 15) return fail(ODX_EINVAL, "X_local must be 16-byte aligned");
@@ -223,9 +230,12 @@ int odx_shard_decide_step(const odx_problem* P, const odx_stepper* S, const odx_
 int odx_shard_fixup(const odx_problem* P, const double* records, int32_t rank, int32_t nranks,
                     double* X_local, int64_t N_local, double* halo, double* step_out,
                     void* workspace, size_t workspace_bytes, void* stream) {
-    if (!P || P->dim < 1 || P->dim > 4) return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
     if (rank < 0 || rank >= nranks || N_local < 1) return fail(ODX_EINVAL, "bad rank / extent");
     if (!records || !X_local) return fail(ODX_EINVAL, "null device buffer");
+    if (dense_problem(P))
+        return dense_shard_fixup(records, rank, X_local, N_local, halo, step_out, workspace,
+                                 workspace_bytes, (cudaStream_t)stream);
+    if (!P || P->dim < 1 || P->dim > 4) return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
     return with_dim(P->dim, [&]<int D>() {
         return shard_fixup_d<D>(records, rank, X_local, N_local, halo, step_out, workspace,
                                 workspace_bytes, (cudaStream_t)stream);

@@ -73,6 +73,8 @@ struct DenseParams {
     int fld;                  // row stride of F in memory: FLD (solve workspace) or DN (ops)
     long long* flist;         // steps the band kernel hands to the warp LU
     unsigned* fcount;         // per iteration (solve) or one slot (ops)
+    long long offset;         // global index of local step 0 (time shards): F = 0 only at 0
+    const double* z0;         // fold: state before the first chunk (null: zero)
 };
 
 // ---- NaN-ignoring row rule over 64 entries held two per lane (_kernels.py:84-95)
@@ -134,7 +136,7 @@ dense_lu_build_kernel(const DenseParams p, int it) {
             if (p.h) p.h[k * DN + r] = hv[h];
         }
         rn = nan_drop_max(rn, warp_row_rule64(hv[0], hv[1]));
-        const bool with_F = (k != 0);
+        const bool with_F = (p.offset + k != 0);
         // A = I - dt w_next Jn and B = I + dt w_prev Jp: identity everywhere
         // the Jacobian row is structurally 0 (dij -/+ dt w * 0.0 == dij), the
         // reference's non-contracted expressions at the DP::ROW_NZ entries
@@ -178,7 +180,7 @@ dense_lu_build_kernel(const DenseParams p, int it) {
         const int sk = warp_lu_factor(W, lane);
         double* Fk = p.F + k * DN * p.fld;
         if (sk >= 0) {
-            if ((unsigned long long)k < bad) bad = (unsigned long long)k;
+            if ((unsigned long long)(p.offset + k) < bad) bad = (unsigned long long)(p.offset + k);
             for (int q = lane; q < DN * DN; q += 32) Fk[(q >> 6) * p.fld + (q & 63)] = 0.0;
             p.c[k * DN + lane] = 0.0;
             p.c[k * DN + lane + 32] = 0.0;
@@ -263,14 +265,14 @@ dense_band_build_kernel(const DenseParams p, int it) {
         double* Fk = p.F + k * DN * p.fld;
         bool handoff = (fr < 0);
         if (fr > 0) {  // singular pivot fr - 1 (no row swap involved)
-            if ((unsigned long long)k < bad) bad = (unsigned long long)k;
+            if ((unsigned long long)(p.offset + k) < bad) bad = (unsigned long long)(p.offset + k);
             for (int q = lane; q < DN * DN; q += 32) Fk[(q >> 6) * p.fld + (q & 63)] = 0.0;
             p.c[k * DN + lane] = 0.0;
             p.c[k * DN + lane + 32] = 0.0;
         } else if (fr == 0) {
             const double c0 = W.c[lane], c1 = W.c[lane + 32];
             bool fin = isfinite(c0) && isfinite(c1);
-            if (k != 0) {
+            if (p.offset + k != 0) {
 #pragma unroll 1
                 for (int pass = 0; pass < 2; pass++) {
                     const int col = lane + 32 * pass;
@@ -487,8 +489,9 @@ __global__ void __launch_bounds__(DTHREADS) dense_fold_kernel(const DenseParams 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < DN) {
-        sm.z[0][tid] = 0.0;  // the state before step 0
-        p.zin[tid] = 0.0;
+        const double z = p.z0 ? p.z0[tid] : 0.0;  // the state before the first chunk
+        sm.z[0][tid] = z;
+        p.zin[tid] = z;
     }
     __syncthreads();
     auto stage_agg = [&](int q, int b) {
@@ -713,6 +716,256 @@ int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, voi
     dense_final_copy_kernel<<<(unsigned)(2 * num_sms()), 256, 0, st>>>(p);
     ODX_CUDA(cudaGetLastError());
     count_launch(launches + 1);
+    return ODX_OK;
+}
+
+
+// =========================================================================
+// Time-sharded d = 64 iteration, host-decided protocol
+// (sharded.ShardedNewton): the local pass builds the rank's elements (halo =
+// the state before local step 0; F = 0 only at global step 0), folds them into
+// chunk aggregates (dense_agg_kernel) and folds those twice more with the
+// same kernel (chunks of chunk aggregates, then one chunk) into the rank
+// aggregate M_r = F_last ... F_first, v_r; record
+// [M_r (64 x 64) | v_r | x_last | rn | sc | step_prev | bad].  The fix-up
+// computes the carry z_r from the gathered records, runs the chunk fold from
+// z_r and the chunk fix-up, and sets the last row to x_last + (M_r z_r + v_r)
+// with the same function that computes rank r+1's carry (bit-identical halo).
+// =========================================================================
+constexpr int SHARD_FAN = 6;  // chunk aggregates composed per CTA in each tree level
+
+struct DenseShardLayout {
+    int C, G;  // chunks; groups of SHARD_FAN chunks (tree level 1)
+    size_t F, c, aggP, aggy, tP[3], ty[3], zg, zin, red, st, flist, fcount, z, dlast, total;
+    explicit DenseShardLayout(long long n) {
+        const int cm = dense_chunks();
+        C = (int)(n < cm ? n : cm);
+        G = (C + SHARD_FAN - 1) / SHARD_FAN;
+        size_t off = 0;
+        auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
+        F = at((size_t)n * DN * FLD * 8);
+        c = at((size_t)n * DN * 8);
+        aggP = at((size_t)C * DN * FLD * 8);
+        aggy = at((size_t)C * DN * 8);
+        // tree levels: level 1 (G entries, kept for the fix-up) in tP[0], later
+        // levels alternate between tP[1] and tP[2]
+        for (int b = 0; b < 3; b++) {
+            const size_t m = (b == 0) ? (size_t)G : (size_t)(G + SHARD_FAN - 1) / SHARD_FAN;
+            tP[b] = at(m * DN * FLD * 8);
+            ty[b] = at(m * DN * 8);
+        }
+        zg = at((size_t)G * DN * 8);
+        zin = at((size_t)C * DN * 8);
+        red = at(4 * 8);
+        st = at(sizeof(DenseState));
+        flist = at((size_t)n * 8);
+        fcount = at(4);
+        z = at(DN * 8);
+        dlast = at(DN * 8);
+        total = off + 256;
+    }
+};
+
+// chunk states inside each group: CTA g starts from the group's state zg[g]
+// and walks its (about SHARD_FAN) chunk aggregates (zin[q] = state before chunk q)
+struct ExpandSmem {
+    double A[DN * FLD];
+    double a[DN];
+    double z[2][DN];
+    uint64_t bar;
+};
+__global__ void __launch_bounds__(DTHREADS) dense_expand_kernel(const DenseParams p,
+                                                                const double* zg) {
+    extern __shared__ __align__(16) unsigned char raw[];
+    ExpandSmem& sm = *reinterpret_cast<ExpandSmem*>(raw);
+    const int tid = threadIdx.x, g = blockIdx.x;
+    // the same split of the C chunks into G groups as tree level 1 (chunk_begin)
+    const int lo = chunk_begin(p.nchunks, (int)gridDim.x, g);
+    const int hi = chunk_begin(p.nchunks, (int)gridDim.x, g + 1);
+    if (tid == 0) {
+        mbar_init(&sm.bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < DN) sm.z[0][tid] = zg[(long long)g * DN + tid];
+    __syncthreads();
+    int zb = 0;
+    for (int q = lo; q < hi; q++) {
+        if (tid < DN) p.zin[(long long)q * DN + tid] = sm.z[zb][tid];
+        if (q + 1 == hi) break;
+        if (tid == 0) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&sm.bar, DN * FLD * 8 + DN * 8);
+            tma_load_1d(sm.A, p.aggP + (long long)q * DN * FLD, DN * FLD * 8, &sm.bar);
+            tma_load_1d(sm.a, p.aggy + (long long)q * DN, DN * 8, &sm.bar);
+        }
+        mbar_wait(&sm.bar, (uint32_t)((q - lo) & 1));
+        matvec64(sm.A, sm.z[zb], sm.a, sm.z[zb ^ 1]);
+        __syncthreads();
+        zb ^= 1;
+    }
+}
+
+// out[r] = v[r] + sum_j M[r, j] z[j] (fixed order, fused multiply-adds): the
+// carry chain of every rank and each rank's exit state use this one function
+__device__ __noinline__ double dense_carry_row(const double* M, const double* v, const double* z,
+                                               int r) {
+    double acc = v[r];
+    for (int j = 0; j < DN; j++) acc = __fma_rn(M[r * DN + j], z[j], acc);
+    return acc;
+}
+
+__global__ void dense_shard_record_kernel(const double* aggP3, const double* aggy3,
+                                          const double* X, long long n,
+                                          const unsigned long long* red, double* rec) {
+    const int tid = threadIdx.x;
+    for (int q = tid; q < DN * DN; q += blockDim.x) rec[q] = aggP3[(q >> 6) * FLD + (q & 63)];
+    if (tid < DN) {
+        rec[DN * DN + tid] = aggy3[tid];
+        rec[DN * DN + DN + tid] = X[(n - 1) * DN + tid];
+    }
+    if (tid == 0) {
+        double* t = rec + DN * DN + 2 * DN;
+        t[0] = bitsd(red[0]);
+        t[1] = bitsd(red[1]);
+        t[2] = __longlong_as_double(0x7ff8000000000000ll);
+        t[3] = (red[3] == ~0ull) ? -1.0 : (double)(long long)red[3];
+    }
+}
+
+__global__ void dense_shard_carry_kernel(const double* recs, int rank, double* halo, double* z_out,
+                                         double* dlast, unsigned long long* red) {
+    constexpr int R = ODX_SHARD_REC(DN);
+    __shared__ double z[DN], t[DN];
+    const int tid = threadIdx.x;
+    if (tid < DN) z[tid] = 0.0;
+    __syncthreads();
+    for (int q = 0; q < rank; q++) {
+        const double* M = recs + (long long)q * R;
+        if (tid < DN) t[tid] = dense_carry_row(M, M + DN * DN, z, tid);
+        __syncthreads();
+        if (tid < DN) z[tid] = t[tid];
+        __syncthreads();
+    }
+    if (tid < DN) {
+        const double* M = recs + (long long)rank * R;
+        z_out[tid] = z[tid];
+        dlast[tid] = dense_carry_row(M, M + DN * DN, z, tid);
+        if (halo && rank > 0) halo[tid] = halo[tid] + z[tid];
+    }
+    if (tid == 0) red[2] = 0ull;
+}
+
+__global__ void dense_shard_finish_kernel(const double* recs, int rank, const double* dlast,
+                                          double* X, long long n, const unsigned long long* red,
+                                          double* step_out) {
+    const int tid = threadIdx.x;
+    const double* xl = recs + (long long)rank * ODX_SHARD_REC(DN) + DN * DN + DN;
+    if (tid < DN) X[(n - 1) * DN + tid] = xl[tid] + dlast[tid];
+    if (tid == 0 && step_out) *step_out = bitsd(red[2]);
+}
+
+size_t dense_shard_workspace(long long n) { return DenseShardLayout(n).total; }
+
+static DenseParams dense_shard_params(const DenseShardLayout& lay, char* base, double* X,
+                                      long long n) {
+    DenseParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.X = X;
+    p.Xalt = X;  // the fix-up updates rows in place (each row read, then written, by one thread)
+    p.N = n;
+    p.F = reinterpret_cast<double*>(base + lay.F);
+    p.fld = FLD;
+    p.c = reinterpret_cast<double*>(base + lay.c);
+    p.aggP = reinterpret_cast<double*>(base + lay.aggP);
+    p.aggy = reinterpret_cast<double*>(base + lay.aggy);
+    p.zin = reinterpret_cast<double*>(base + lay.zin);
+    p.red = reinterpret_cast<unsigned long long*>(base + lay.red);
+    p.st = reinterpret_cast<DenseState*>(base + lay.st);
+    p.nchunks = lay.C;
+    p.flist = reinterpret_cast<long long*>(base + lay.flist);
+    p.fcount = reinterpret_cast<unsigned*>(base + lay.fcount);
+    return p;
+}
+
+int dense_shard_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
+                      const double* X_local, long long n, long long offset, double* record,
+                      void* ws, size_t ws_bytes, cudaStream_t st) {
+    const DenseShardLayout lay(n);
+    if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "shard workspace");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    DenseParams p = dense_shard_params(lay, base, const_cast<double*>(X_local), n);
+    p.prob = pp;
+    p.sc = sc;
+    p.x0 = halo;
+    p.offset = offset;
+    p.max_iters = 1;
+    dense_init_kernel<<<1, 32, 0, st>>>(p.st, p.red, 1);
+    ODX_CUDA(cudaMemsetAsync(p.fcount, 0, 4, st));
+    auto kb = dense_band_build_kernel<AllenCahnRows>;
+    auto k1 = dense_lu_build_kernel<AllenCahnRows, true>;
+    if (int rc = set_smem(k1, lu_smem())) return rc;
+    if (int rc = set_smem(dense_agg_kernel, sizeof(AggSmem))) return rc;
+    int per_sm = 0;
+    ODX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, BAND_WARPS * 32, 0));
+    long long gb = (long long)(per_sm < 1 ? 1 : per_sm) * num_sms();
+    if (gb > (n + BAND_WARPS - 1) / BAND_WARPS) gb = (n + BAND_WARPS - 1) / BAND_WARPS;
+    kb<<<(unsigned)gb, BAND_WARPS * 32, 0, st>>>(p, 0);
+    k1<<<(unsigned)num_sms(), LU_WARPS * 32, lu_smem(), st>>>(p, 0);
+    // chunk aggregates, then a tree of aggregates of SHARD_FAN consecutive
+    // ones (level 1 is kept: the fix-up's group states start from it) down to
+    // the rank's
+    dense_agg_kernel<<<lay.C, DTHREADS, sizeof(AggSmem), st>>>(p);
+    int launches = 5;
+    DenseParams q = p;
+    const double* srcP = p.aggP;
+    const double* srcy = p.aggy;
+    int cnt = lay.C, b = 0;
+    do {
+        q.F = const_cast<double*>(srcP);
+        q.c = const_cast<double*>(srcy);
+        q.N = cnt;
+        q.nchunks = (cnt + SHARD_FAN - 1) / SHARD_FAN;
+        q.aggP = reinterpret_cast<double*>(base + lay.tP[b]);
+        q.aggy = reinterpret_cast<double*>(base + lay.ty[b]);
+        dense_agg_kernel<<<q.nchunks, DTHREADS, sizeof(AggSmem), st>>>(q);
+        launches++;
+        srcP = q.aggP;
+        srcy = q.aggy;
+        cnt = q.nchunks;
+        b = (b == 1) ? 2 : 1;  // level 1 stays in tP[0]; later levels alternate
+    } while (cnt > 1);
+    dense_shard_record_kernel<<<1, 256, 0, st>>>(srcP, srcy, X_local, n, p.red, record);
+    ODX_CUDA(cudaGetLastError());
+    count_launch(launches + 1);
+    return ODX_OK;
+}
+
+int dense_shard_fixup(const double* records, int rank, double* X_local, long long n, double* halo,
+                      double* step_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const DenseShardLayout lay(n);
+    if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "shard workspace");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    DenseParams p = dense_shard_params(lay, base, X_local, n);
+    double* z = reinterpret_cast<double*>(base + lay.z);
+    double* dlast = reinterpret_cast<double*>(base + lay.dlast);
+    p.z0 = z;
+    if (int rc = set_smem(dense_fixup_kernel, sizeof(FixSmem))) return rc;
+    if (int rc = set_smem(dense_fold_kernel, sizeof(FoldSmem))) return rc;
+    if (int rc = set_smem(dense_expand_kernel, sizeof(ExpandSmem))) return rc;
+    dense_shard_carry_kernel<<<1, 64, 0, st>>>(records, rank, halo, z, dlast, p.red);
+    // group states: fold of the level-1 aggregates from the carry (one CTA, G
+    // steps), then every group expands its SHARD_FAN chunk states in parallel
+    DenseParams f = p;
+    f.aggP = reinterpret_cast<double*>(base + lay.tP[0]);
+    f.aggy = reinterpret_cast<double*>(base + lay.ty[0]);
+    f.zin = reinterpret_cast<double*>(base + lay.zg);
+    f.nchunks = lay.G;
+    dense_fold_kernel<<<1, DTHREADS, sizeof(FoldSmem), st>>>(f);
+    dense_expand_kernel<<<lay.G, DTHREADS, sizeof(ExpandSmem), st>>>(p, f.zin);
+    dense_fixup_kernel<<<lay.C, DTHREADS, sizeof(FixSmem), st>>>(p, 0);
+    dense_shard_finish_kernel<<<1, 64, 0, st>>>(records, rank, dlast, X_local, n, p.red, step_out);
+    ODX_CUDA(cudaGetLastError());
+    count_launch(6);
     return ODX_OK;
 }
 

@@ -184,3 +184,53 @@ def test_emulated_time_sharding_long(oracle, case, mode):
     assert np.array_equal(fin, np.isfinite(X).all(axis=1))
     scale = max(1.0, float(np.abs(ref["X"][fin]).max()))
     assert np.abs(X[fin] - ref["X"][fin]).max() <= 1e-9 * scale
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_emulated_time_sharding_dense(golden_baseline, R):
+    """cfg4's d = 64 Allen-Cahn path split along time (two-pass protocol,
+    rank aggregate M_r = F_last ... F_first from the chunk aggregates): the
+    N = 4096 run converges like the unsharded oracle (golden cfg4s_*)."""
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200.configs import CONFIGS
+    cfg = CONFIGS[4]
+    n = 4096
+    prob = pkg.allen_cahn(n=cfg.dim, eps=cfg.params[0], dx=cfg.params[1], u0=cfg.x0s()[0],
+                          tf=n * cfg.dt)
+    st = pkg.get_stepper(cfg.stepper, prob)
+    guess = np.tile(prob.x0, (n, 1))
+    X, res = _emulate(pkg, prob, st, cfg.dt, guess, R, cfg.max_iters, cfg.step_tol,
+                      cfg.abort_nonfinite, "two_pass")
+    g = golden_baseline
+    assert res["status"] == int(g["cfg4s_status"])
+    assert abs(res["iters"] - int(g["cfg4s_iters"])) <= 1
+    ref = g["cfg4s_X_sub"]
+    scale = max(1.0, float(np.abs(ref).max()))
+    assert np.abs(X[::32] - ref).max() <= 1e-9 * scale
+    h = np.array(res["hist"])
+    hr = g["cfg4s_hist"][:len(h)]
+    assert (np.abs(h - hr) <= 1e-7 * hr + 1e-9 * hr[0]).all()
+
+
+def test_emulated_time_sharding_dense_full_size():
+    """cfg4 at its full N = 65536 over 8 emulated ranks, 3 fixed iterations
+    (diverging iterates up to ~1e19): against the unsharded GPU solve, which
+    tests/test_gpu_parity.py pins to the oracle."""
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200.configs import CONFIGS
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    cfg = CONFIGS[4]
+    n = cfg.n_steps
+    prob = pkg.allen_cahn(n=cfg.dim, eps=cfg.params[0], dx=cfg.params[1], u0=cfg.x0s()[0],
+                          tf=n * cfg.dt)
+    st = pkg.get_stepper(cfg.stepper, prob)
+    guess = np.tile(prob.x0, (n, 1))
+    X, res = _emulate(pkg, prob, st, cfg.dt, guess, 8, 3, 0.0, False, "two_pass")
+    conf = pkg.NewtonConfig(max_iters=3, abort_on_nonfinite=False)
+    ref = solve_batch(prob, st, cfg.dt, prob.x0[None], None, conf)
+    R = ref.states[0]
+    fin = np.isfinite(R).all(axis=1)
+    assert np.array_equal(fin, np.isfinite(X).all(axis=1))
+    scale = max(1.0, float(np.abs(R[fin]).max()))
+    assert np.abs(X[fin] - R[fin]).max() <= 1e-9 * scale
+    assert res["iters"] == int(ref.iterations_run[0]) and res["status"] == int(ref.status[0])
