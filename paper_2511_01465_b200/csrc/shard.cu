@@ -102,7 +102,10 @@ int shard_step_d(const odx_problem* P, const odx_stepper* S, const double* recor
         reinterpret_cast<unsigned long long*>(base + lay.red), reinterpret_cast<int*>(base + lay.stop));
     ODX_CUDA(cudaGetLastError());
     count_launch(1);
-    return shard_local_dispatch(P, S, dt, halo, X_local, n, offset, record, ws, ws_bytes, st, 1);
+    // the pass builds iteration it+1's elements: never applied when it+1 is
+    // the last iteration of the decision's budget
+    const int mode = (dec && it + 1 == dec->max_iters) ? 2 : 1;
+    return shard_local_dispatch(P, S, dt, halo, X_local, n, offset, record, ws, ws_bytes, st, mode);
 }
 
 template <int D>

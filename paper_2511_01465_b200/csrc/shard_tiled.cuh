@@ -276,6 +276,7 @@ struct ShardFusedParams {
     const int* stop;       // set by the carry / decision pass: skip the pass
     long long n, offset, ntiles;
     int nch;
+    int store;             // 0: the built elements are never applied (last pass): not stored
 };
 
 template <int D, int THREADS, int ITEMS>
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
             if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(e.c));
             if (sing && (unsigned long long)(fp.offset + k) < bad)
                 bad = (unsigned long long)(fp.offset + k);
-            st_elem<D>(&sm.out[(tid * ITEMS + q) * E], e);
+            if (fp.store) st_elem<D>(&sm.out[(tid * ITEMS + q) * E], e);
             if (nh)
                 compose<D>(nagg, e, nagg);
             else {
@@ -536,8 +537,10 @@ __global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFuse
         fence_proxy_async_smem();  // staged elements -> the bulk store (async proxy)
         __syncthreads();  // (2) new elements staged, tile aggregates published
         if (tid == 0) {
-            tma_store_1d(fp.el + base * E, sm.out, (uint32_t)(rows * E * 8));
-            tma_store_commit();
+            if (fp.store) {
+                tma_store_1d(fp.el + base * E, sm.out, (uint32_t)(rows * E * 8));
+                tma_store_commit();
+            }
             for (int q = 0; q < NW; q++) {
                 if (!s_nh[q]) continue;
                 Elem<D> a;
@@ -639,6 +642,7 @@ int shard_tiled_local(const ProbParams& pp, const StepCoefs& sc, const double* h
         fp.offset = offset;
         fp.ntiles = ntiles;
         fp.nch = nch;
+        fp.store = (fused == 1) ? 1 : 0;  // 2: the last pass of a fixed-length solve
         const size_t smem = sizeof(ShardFusedSmem<D, THREADS, ITEMS>);
         auto kf = shard_fused_kernel<P, KIND, S, THREADS, ITEMS>;
         int occ = 0;
@@ -710,8 +714,10 @@ int fused_tiled_solve(const SolveParams& p, void* ws, size_t ws_bytes, cudaStrea
             reinterpret_cast<unsigned long long*>(base + lay.red),
             reinterpret_cast<int*>(base + lay.stop));
         count_launch(1);
+        // the pass of iteration it builds iteration it+1's elements; at
+        // it+1 == max_iters they are never applied (only rn is needed)
         if (int rc = shard_tiled_local<P, KIND, S>(p.prob, p.sc, p.x0, p.X, p.N, 0, rec, ws,
-                                                   ws_bytes, st, 1))
+                                                   ws_bytes, st, it + 1 == p.max_iters ? 2 : 1))
             return rc;
     }
     fused_solve_finish_kernel<<<1, 1, 0, st>>>(state, p.iters, p.status, p.sidx);
