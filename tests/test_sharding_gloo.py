@@ -30,10 +30,21 @@ CASES = {
     "lorenz_cfg1": (6, (10.0, 28.0, 8.0 / 3.0), "rk4", [1.0, 1.0, 1.0], 1024, 0.01, 100, 1e-10,
                     True),
     "logistic_converge": (0, (1.0, 1.0), "rk4", [0.1], 1000, 1e-2, 11, 1e-10, True),
+    # the d = 64 record (64 x 64 rank aggregate): cfg4's Allen-Cahn problem and
+    # x0, N = 256, until converged
+    "allen_cahn_cfg4": (7, (0.01, 0.015625), "backward_euler", "cfg4_x0", 256, 1e-3, 20, 1e-10,
+                        True),
 }
 # initial guess per case (default: replicate x0); the logistic case uses the
 # reference's own convergent "ones" guess (tests/test_acceptance.py crit 3)
 GUESS_ONES = {"logistic_converge"}
+
+
+def _x0(x0):
+    if isinstance(x0, str):  # a golden fixture entry
+        from pathlib import Path
+        return np.load(Path(__file__).resolve().parent / "golden" / "baseline.npz")[x0]
+    return np.asarray(x0, np.float64)
 
 
 def _worker(rank, world, port, case, q, fused=False):
@@ -45,7 +56,7 @@ def _worker(rank, world, port, case, q, fused=False):
         from oracle import oracle as O
         from paper_2511_01465_b200.sharded import ShardedNewton, chunk_bounds
         pid, params, sname, x0, n, dt, max_iters, step_tol, abort = CASES[case]
-        x0 = np.asarray(x0, np.float64)
+        x0 = _x0(x0)
         off, nl = chunk_bounds(n, world, rank)
         guess = np.ones((n, x0.shape[0])) if case in GUESS_ONES else np.tile(x0, (n, 1))
         halo = x0 if rank == 0 else guess[off - 1]
@@ -86,7 +97,7 @@ def test_time_sharded_protocol_gloo(oracle, case, fused):
     outs = [r[3] for r in res]
     assert outs[0]["status"] == outs[1]["status"] and outs[0]["iters"] == outs[1]["iters"]
     pid, params, sname, x0, n, dt, max_iters, step_tol, abort = CASES[case]
-    x0 = np.asarray(x0, np.float64)
+    x0 = _x0(x0)
     guess = np.ones((n, x0.shape[0])) if case in GUESS_ONES else np.tile(x0, (n, 1))
     ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), x0, guess, dt,
                        max_iters, step_tol=step_tol, abort_nonfinite=abort)
