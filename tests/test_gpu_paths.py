@@ -78,3 +78,21 @@ def test_long_trajectory_routes(case, route):
     assert r["err"] <= 1e-9, r
     assert r["hrel"] <= 1e-7, r
     assert abs(r["iters"] - r["ref_iters"]) <= 1
+
+
+def test_fused_tiled_deterministic():
+    """The fused tiled route twice on the same input gives bit-identical
+    iterates and histories: no value depends on CTA scheduling (the only
+    atomics are order-independent max / min reductions)."""
+    import numpy as np
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    n, dt = 1 << 22, 1e-3
+    prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
+    st = pkg.get_stepper("rk4", prob)
+    conf = pkg.NewtonConfig(max_iters=4, abort_on_nonfinite=False)
+    guess = np.tile(prob.x0, (1, n, 1)) + 1e-3
+    a = solve_batch(prob, st, dt, prob.x0[None], guess, conf)
+    b = solve_batch(prob, st, dt, prob.x0[None], guess, conf)
+    assert np.array_equal(a.states, b.states, equal_nan=True)
+    assert np.array_equal(a.residual_history, b.residual_history, equal_nan=True)
