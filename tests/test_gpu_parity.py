@@ -463,10 +463,11 @@ def test_host_buffer_path_matches_device_path(pkg):
 
 # N values straddling every kernel-selection boundary for d = 2: the resident
 # CTA (N <= 2048), the grid-resident wave (2-item tiles up to 37888 steps,
-# 4-item tiles up to a full co-resident wave) and the streaming kernel beyond;
-# tiny and ragged sizes included.
-_BOUNDARY_N = [1, 2, 3, 255, 257, 2047, 2048, 2049, 4097, 37888, 37889, 65537, 200_003,
-               240_001, 300_007]
+# 4-item tiles up to a full co-resident wave), the small-tile streaming kernel
+# up to 151552 steps (d = 2) and the fused tiled passes beyond; tiny and
+# ragged sizes included.
+_BOUNDARY_N = [1, 2, 3, 255, 257, 2047, 2048, 2049, 4097, 37888, 37889, 65537, 100_003,
+               151_551, 151_553, 200_003, 240_001, 300_007]
 
 
 @pytest.mark.parametrize("n", _BOUNDARY_N)
