@@ -230,7 +230,8 @@ class Workload:
 
 
 class TimeShardedWorkload:
-    """cfg 5 at N > 1 GPUs: one trajectory split along time (sharded.py)."""
+    """One trajectory split along time over the ranks (sharded.py): cfg 5 (the
+    device-decided fused protocol) or cfg 4 (d = 64, two-pass protocol)."""
 
     def __init__(self, cid: int, iters: int, rank: int, world: int):
         import torch
@@ -245,7 +246,11 @@ class TimeShardedWorkload:
         self.B, self.d = 1, cfg.dim
         self.iters = iters
         x0 = cfg.x0s()[0]
-        self.prob = pkg.van_der_pol(mu=cfg.params[0], x0=x0, tf=self.n_total * cfg.dt)
+        if cfg.problem == "vdp":
+            self.prob = pkg.van_der_pol(mu=cfg.params[0], x0=x0, tf=self.n_total * cfg.dt)
+        else:
+            self.prob = pkg.allen_cahn(n=cfg.dim, eps=cfg.params[0], dx=cfg.params[1], u0=x0,
+                                       tf=self.n_total * cfg.dt)
         self.stepper = pkg.get_stepper(cfg.stepper, self.prob)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.guess = torch.from_numpy(x0).to(dev)[None, :].expand(self.n, self.d).contiguous()
@@ -521,22 +526,27 @@ def main():
             except Exception as exc:  # report, never hide
                 extra[f"cfg{ocid}"] = {"error": f"{type(exc).__name__}: {exc}"}
 
-    if not args.no_extra and world > 1 and cid != 5:
-        # cfg5's one trajectory split along time over the N ranks (device-decided
-        # protocol, one NCCL all-gather per iteration): strong scaling against
-        # the N = 1 run's configs["cfg5_..."] entry (same flush, same iterations)
-        try:
-            tw = TimeShardedWorkload(5, args.iters, rank, world)
-            td, tl = time_steps(tw, 3, 2, flush)
-            tms = reduce_max(sum(td), world) / len(td)
-            extra["cfg5_time_sharded"] = {
-                "ranks": world, "fixed_iters": args.iters, "ms": round(tms, 4),
-                "newton_steps_per_s": tw.n_total * args.iters / (tms * 1e-3),
-                "scaling": "strong", "gpu_launches_rank0": tl}
-            del tw
-            torch.cuda.empty_cache()
-        except Exception as exc:  # report, never hide
-            extra["cfg5_time_sharded"] = {"error": f"{type(exc).__name__}: {exc}"}
+    if not args.no_extra and world > 1:
+        # cfg5's and cfg4's one trajectory split along time over the N ranks
+        # (one NCCL all-gather per iteration): strong scaling against the N = 1
+        # run's configs["cfg5_..."] / ["cfg4_..."] entries (same flush, same
+        # iterations)
+        for tcid in (5, 4):
+            if tcid == cid:
+                continue
+            key = f"cfg{tcid}_time_sharded"
+            try:
+                tw = TimeShardedWorkload(tcid, args.iters, rank, world)
+                td, tl = time_steps(tw, 3, 2, flush)
+                tms = reduce_max(sum(td), world) / len(td)
+                extra[key] = {
+                    "ranks": world, "fixed_iters": args.iters, "ms": round(tms, 4),
+                    "newton_steps_per_s": tw.n_total * args.iters / (tms * 1e-3),
+                    "scaling": "strong", "gpu_launches_rank0": tl}
+                del tw
+                torch.cuda.empty_cache()
+            except Exception as exc:  # report, never hide
+                extra[key] = {"error": f"{type(exc).__name__}: {exc}"}
 
     cpu = None
     if rank == 0 and not args.no_cpu:

@@ -17,9 +17,12 @@ with socket.socket() as s:
 os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
 buf = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
-tw = bench.TimeShardedWorkload(5, 10, 0, 1)
-td, tl = bench.time_steps(tw, 3, 2, lambda: bench.flush_l2(buf))
-it, st, ix = tw.outcome()
-print(f"cfg5 time-sharded x1: {sum(td) / len(td):.3f} ms per solve, launches {tl}, "
-      f"iters {it[0]} status {st[0]}")
+for cid in (5, 4):
+    tw = bench.TimeShardedWorkload(cid, 10, 0, 1)
+    td, tl = bench.time_steps(tw, 3, 2, lambda: bench.flush_l2(buf))
+    it, st, ix = tw.outcome()
+    print(f"cfg{cid} time-sharded x1: {sum(td) / len(td):.3f} ms per solve, launches {tl}, "
+          f"iters {it[0]} status {st[0]}")
+    del tw
+    torch.cuda.empty_cache()
 dist.destroy_process_group()
