@@ -228,7 +228,56 @@ static int make_solve_params(const odx_problem* P, const odx_stepper* S, const d
 }
 
 static int solve_impl(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
+                      size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
+
+// B > 1 trajectories longer than the batched kernel takes (and the d = 64
+// path, one trajectory per launch): the single-trajectory solve per
+// trajectory, back to back on the stream, sharing the workspace.  A
+// trajectory whose rows are not 16-byte aligned (odd N * d) is staged through
+// an aligned copy at the front of the workspace (the streaming kernels move
+// rows with TMA).
+static int solve_each(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
                       size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
+    const long long d = P->dim;
+    const size_t xbytes = (size_t)p.N * (size_t)d * 8;
+    const size_t stage = align_up(xbytes, 256) + 256;
+    SolveParams q = p;
+    q.B = 1;
+    size_t one = 0;
+    if (int rc = solve_impl(P, S, q, nullptr, 0, st, true, &one)) return rc;
+    if (query) {
+        *need = stage + one;
+        return ODX_OK;
+    }
+    if (!ws || ws_bytes < stage + one) return fail(ODX_EWORKSPACE, "workspace too small");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    double* scratch = reinterpret_cast<double*>(base);
+    void* ws1 = base + stage - 256;
+    const size_t ws1_bytes = ws_bytes - (size_t)(static_cast<char*>(ws1) - static_cast<char*>(ws));
+    const long long H = p.max_iters + 1;
+    for (long long b = 0; b < p.B; b++) {
+        double* Xb = p.X + b * p.N * d;
+        const bool aligned = (reinterpret_cast<uintptr_t>(Xb) & 15) == 0;
+        q.x0 = p.x0 + b * d;
+        q.X = aligned ? Xb : scratch;
+        q.hist = p.hist ? p.hist + b * H : nullptr;
+        q.shist = p.shist ? p.shist + b * H : nullptr;
+        q.iters = p.iters + b;
+        q.status = p.status + b;
+        q.sidx = p.sidx + b;
+        if (!aligned) ODX_CUDA(cudaMemcpyAsync(scratch, Xb, xbytes, cudaMemcpyDeviceToDevice, st));
+        if (int rc = solve_impl(P, S, q, ws1, ws1_bytes, st, false, nullptr)) return rc;
+        if (!aligned) ODX_CUDA(cudaMemcpyAsync(Xb, scratch, xbytes, cudaMemcpyDeviceToDevice, st));
+    }
+    return ODX_OK;
+}
+
+static int solve_impl(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
+                      size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
+    const bool long_traj = dense_supported(P, S) || p.N > resident_max_steps(P->dim);
+    const bool misaligned = !query && (reinterpret_cast<uintptr_t>(p.X) & 15) != 0;
+    if (long_traj && (p.B > 1 || misaligned))
+        return solve_each(P, S, p, ws, ws_bytes, st, query, need);
     if (dense_supported(P, S)) return dense_solve(P, S, p, ws, ws_bytes, st, query, need);
     int rc = with_small_problem(P->problem_id, P->dim, SolveFn{S, &p, ws, ws_bytes, st, query, need});
     if (rc == ODX_EUNSUPPORTED && odx_last_error()[0] == 0)

@@ -39,6 +39,10 @@ int kernel_occupancy(const void* kern, int threads, size_t smem, int* per_sm);
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// longest trajectory the batched (one CTA per trajectory) solve takes:
+// 256 threads x (8 steps for d <= 3, 4 for d = 4) — solve_small_launch.cuh
+constexpr long long resident_max_steps(int d) { return 256LL * (d <= 3 ? 8 : 4); }
+
 // Carves a workspace into aligned sub-buffers (dry run when base is null).
 struct Carver {
     char* base;

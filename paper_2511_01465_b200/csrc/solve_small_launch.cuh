@@ -255,6 +255,7 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
                 size_t* need) {
     constexpr int D = P::D;
     constexpr int RI = (D <= 3) ? 8 : 4;   // items per thread, resident
+    static_assert(256LL * RI == resident_max_steps(D), "resident limit");
     const bool resident = p.N <= 256LL * RI;
     constexpr int WI = ws_items<D>();
     const bool small_ws = p.N < 128LL * WI * 296;  // keep >= 2 tiles per SM

@@ -733,3 +733,53 @@ def test_parareal_vs_host_restatement(pkg, oracle):
     assert res.trajectory.n_steps == cfg.n_fine_total
     with pytest.raises(ValueError):
         pkg.solve_parareal(prob, pkg.get_stepper("backward_euler", prob), fine, cfg)
+
+
+@pytest.mark.parametrize("case", [
+    # (problem, stepper, B, N): batches of trajectories longer than the batched
+    # kernel takes run one trajectory after another; odd N * d rows of the
+    # second trajectory are staged through an aligned copy
+    ("vdp1", "rk4", 3, 100_003),
+    ("logistic", "rk4", 2, 300_001),
+    ("vdp10", "backward_euler", 2, 200_001),
+])
+def test_batched_long_trajectories(pkg, oracle, case):
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    name, sname, B, n = case
+    dt = 1e-3
+    if name == "logistic":
+        dt = 1e-5
+        prob = pkg.problems.logistic(tf=n * dt)
+        pid, params = 0, (1.0, 1.0)
+        x0s = np.array([[0.1], [0.3]])
+    else:
+        mu = 1.0 if name == "vdp1" else 10.0
+        prob = pkg.van_der_pol(mu=mu, x0=(2.0, 0.0), tf=n * dt)
+        pid, params = 1, (mu,)
+        x0s = np.array([[2.0, 0.0], [2.0, 1e-3], [1.999, 0.0]])[:B]
+    st = pkg.get_stepper(sname, prob)
+    conf = pkg.NewtonConfig(max_iters=3, abort_on_nonfinite=False)
+    r = solve_batch(prob, st, dt, x0s, None, conf)
+    for b in range(B):
+        ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), x0s[b],
+                           np.tile(x0s[b], (n, 1)), dt, 3, abort_nonfinite=False)
+        assert int(r.iterations_run[b]) == ref["iters"] and int(r.status[b]) == ref["status"]
+        scaled_close(r.residual_history[b], ref["hist"], 1e-7, f"b={b} hist")
+        scaled_close(r.states[b], ref["X"], TOL, f"b={b} states")
+
+
+def test_batched_dense_trajectories(pkg, golden_baseline):
+    """d = 64: two trajectories (the dense path solves one per launch)."""
+    from paper_2511_01465_b200.configs import CONFIGS
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    cfg = CONFIGS[4]
+    n = 512
+    prob = pkg.allen_cahn(n=cfg.dim, eps=cfg.params[0], dx=cfg.params[1], u0=cfg.x0s()[0],
+                          tf=n * cfg.dt)
+    st = pkg.get_stepper(cfg.stepper, prob)
+    conf = pkg.NewtonConfig(max_iters=3, abort_on_nonfinite=False)
+    x0s = np.stack([prob.x0, prob.x0])
+    r = solve_batch(prob, st, cfg.dt, x0s, None, conf)
+    g = golden_baseline
+    for b in range(2):
+        scaled_close(r.states[b], g["cfg4t_X"], TOL, f"b={b} iterate 3")
