@@ -125,7 +125,9 @@ int64_t     odx_launch_count(void);
  *   scaled_hist[b*(max_iters+1)+it] = max|ce| (implicit) or == hist (explicit)
  *   iters[b]   = iterations_run, status[b] = ODX_ST_*, status_index[b] = the
  *   iteration (NONFINITE) or block index (SINGULAR), -1 otherwise.
- * hist / scaled_hist may be NULL.  Workspace: odx_solve_workspace_bytes().   */
+ * hist / scaled_hist may be NULL.  Workspace: odx_solve_workspace_bytes().
+ * Trajectories of up to 2048 steps (1024 for d = 4) run one CTA each in one
+ * launch; longer ones (and d = 64) run one after another on the stream.      */
 size_t odx_solve_workspace_bytes(const odx_problem* P, const odx_stepper* S,
                                  int64_t B, int64_t N, const odx_newton_cfg* C);
 int odx_solve(const odx_problem* P, const odx_stepper* S,
