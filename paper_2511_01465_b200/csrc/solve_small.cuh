@@ -500,6 +500,10 @@ grid_resident_kernel(const GridResParams gp) {
                 for (int q = 0; q < NW; q++) s2 = fmax(s2, sm.redd[2][q]);
                 if (s2 > 0.0) atomicMax(red - 4 + 2, dbits(s2));
             }
+        }
+        // the tile aggregate on another warp, alongside thread 0's reductions
+        // (the barrier's opening __syncthreads orders both before the arrival)
+        if (tid == (NW > 1 ? 32 : 0)) {
             if (do_scan) {
                 Elem<D> A;
                 bool A_has = false;
