@@ -46,7 +46,13 @@ int add_op(double* X, const double* U, long long n, int d, cudaStream_t st);
 int dense_supported(const odx_problem* P, const odx_stepper* S);
 int dense_shard_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
                       const double* X_local, long long n, long long offset, double* record,
-                      void* ws, size_t ws_bytes, cudaStream_t st);
+                      void* ws, size_t ws_bytes, cudaStream_t st, bool device_decided);
+int dense_shard_decide_step(const double* records, int rank, int nranks, int it, int max_iters,
+                            int abort_nonfinite, double rtol, double stol, double* hist,
+                            double* shist, long long* state, const ProbParams& pp,
+                            const StepCoefs& sc, double* halo, double* X_local, long long n,
+                            long long offset, double* record, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
 int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
                 size_t ws_bytes, cudaStream_t st, bool query, size_t* need);
 int dense_build_op(const odx_problem* P, const odx_stepper* S, const StepCoefs& sc,
@@ -353,6 +359,21 @@ int build_common_offset(const odx_problem* P, const odx_stepper* S, int kind, co
     return with_small_problem(P->problem_id, P->dim, fn);
 }
 
+// the d = 64 shard's device-decided step (shard.cu validates)
+int shard_dense_decide_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
+                                const odx_newton_cfg* C, const double* records, int rank,
+                                int nranks, int it, double* halo, double* X_local, long long n,
+                                long long offset, double* record, double* hist, double* shist,
+                                long long* state, void* ws, size_t ws_bytes, cudaStream_t st) {
+    ProbParams pp;
+    StepCoefs sc;
+    if (!fill_params(P, pp)) return fail(ODX_EINVAL, "bad problem parameters");
+    if (!fill_coefs(S, dt, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
+    return dense_shard_decide_step(records, rank, nranks, it, C->max_iters, C->abort_nonfinite,
+                                   C->residual_tol, C->step_tol, hist, shist, state, pp, sc, halo,
+                                   X_local, n, offset, record, ws, ws_bytes, st);
+}
+
 // one rank's local pass of the time-sharded iteration (shard.cu validates)
 int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
                          const double* halo, const double* X_local, long long n, long long offset,
@@ -363,7 +384,7 @@ int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
     if (!fill_coefs(S, dt, sc)) return fail(ODX_EINVAL, "bad stepper descriptor");
     if (dense_supported(P, S)) {
         if (fused) return fail(ODX_EUNSUPPORTED, "the d = 64 shard runs the two-pass protocol");
-        return dense_shard_local(pp, sc, halo, X_local, n, offset, record, ws, ws_bytes, st);
+        return dense_shard_local(pp, sc, halo, X_local, n, offset, record, ws, ws_bytes, st, false);
     }
     ShardLocalFn fn{S, &pp, &sc, halo, X_local, n, offset, record, ws, ws_bytes, st, fused};
     return with_small_problem(P->problem_id, P->dim, fn);

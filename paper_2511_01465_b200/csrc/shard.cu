@@ -39,7 +39,13 @@ int shard_local_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
 int dense_supported(const odx_problem* P, const odx_stepper* S);
 size_t dense_shard_workspace(long long n);
 int dense_shard_fixup(const double* records, int rank, double* X_local, long long n, double* halo,
-                      double* step_out, void* ws, size_t ws_bytes, cudaStream_t st);
+                      double* step_out, void* ws, size_t ws_bytes, cudaStream_t st,
+                      bool device_decided);
+int shard_dense_decide_dispatch(const odx_problem* P, const odx_stepper* S, double dt,
+                                const odx_newton_cfg* C, const double* records, int rank,
+                                int nranks, int it, double* halo, double* X_local, long long n,
+                                long long offset, double* record, double* hist, double* shist,
+                                long long* state, void* ws, size_t ws_bytes, cudaStream_t st);
 inline bool dense_problem(const odx_problem* P) {
     return P && P->problem_id == ODX_PROB_ALLEN_CAHN && P->dim == 64;
 }
@@ -209,6 +215,17 @@ int odx_shard_decide_step(const odx_problem* P, const odx_stepper* S, const odx_
                           double dt, double* record, double* hist, double* scaled_hist,
                           int64_t* state, void* workspace, size_t workspace_bytes,
                           void* stream) {
+    if (P && S && C && dense_supported(P, S)) {
+        if (C->max_iters < 1) return fail(ODX_EINVAL, "max_iters must be >= 1");
+        if (rank < 0 || rank >= nranks || N_local < 1 || offset < 0 || it < 0 || it > C->max_iters)
+            return fail(ODX_EINVAL, "bad rank / extent / iteration");
+        if (!records || !halo || !X_local || !record || !state)
+            return fail(ODX_EINVAL, "null device buffer");
+        return shard_dense_decide_dispatch(P, S, dt, C, records, rank, nranks, it, halo, X_local,
+                                           N_local, offset, record, hist, scaled_hist,
+                                           reinterpret_cast<long long*>(state), workspace,
+                                           workspace_bytes, (cudaStream_t)stream);
+    }
     if (!P || !S || P->dim < 1 || P->dim > 4 || dense_supported(P, S))
         return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
     if (!C || C->max_iters < 1) return fail(ODX_EINVAL, "max_iters must be >= 1");
@@ -237,7 +254,7 @@ int odx_shard_fixup(const odx_problem* P, const double* records, int32_t rank, i
     if (!records || !X_local) return fail(ODX_EINVAL, "null device buffer");
     if (dense_problem(P))
         return dense_shard_fixup(records, rank, X_local, N_local, halo, step_out, workspace,
-                                 workspace_bytes, (cudaStream_t)stream);
+                                 workspace_bytes, (cudaStream_t)stream, false);
     if (!P || P->dim < 1 || P->dim > 4) return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
     return with_dim(P->dim, [&]<int D>() {
         return shard_fixup_d<D>(records, rank, X_local, N_local, halo, step_out, workspace,

@@ -736,7 +736,8 @@ constexpr int SHARD_FAN = 6;  // chunk aggregates composed per CTA in each tree 
 
 struct DenseShardLayout {
     int C, G;  // chunks; groups of SHARD_FAN chunks (tree level 1)
-    size_t F, c, aggP, aggy, tP[3], ty[3], zg, zin, red, st, flist, fcount, z, dlast, total;
+    size_t F, c, aggP, aggy, tP[3], ty[3], zg, zin, red, st, flist, fcount, z, dlast, halt, stepv,
+        total;
     explicit DenseShardLayout(long long n) {
         const int cm = dense_chunks();
         C = (int)(n < cm ? n : cm);
@@ -762,6 +763,8 @@ struct DenseShardLayout {
         fcount = at(4);
         z = at(DN * 8);
         dlast = at(DN * 8);
+        halt = at(8);   // device-decided protocol: the solve has stopped
+        stepv = at(8);  // this rank's max|dx| of the last fix-up
         total = off + 256;
     }
 };
@@ -778,6 +781,7 @@ __global__ void __launch_bounds__(DTHREADS) dense_expand_kernel(const DenseParam
                                                                 const double* zg) {
     extern __shared__ __align__(16) unsigned char raw[];
     ExpandSmem& sm = *reinterpret_cast<ExpandSmem*>(raw);
+    if (p.st && p.st->stopped) return;
     const int tid = threadIdx.x, g = blockIdx.x;
     // the same split of the C chunks into G groups as tree level 1 (chunk_begin)
     const int lo = chunk_begin(p.nchunks, (int)gridDim.x, g);
@@ -816,8 +820,10 @@ __device__ __noinline__ double dense_carry_row(const double* M, const double* v,
 
 __global__ void dense_shard_record_kernel(const double* aggP3, const double* aggy3,
                                           const double* X, long long n,
-                                          const unsigned long long* red, double* rec) {
+                                          const unsigned long long* red, const int* halt,
+                                          const double* step_in, double* rec) {
     const int tid = threadIdx.x;
+    if (halt && *halt) return;
     for (int q = tid; q < DN * DN; q += blockDim.x) rec[q] = aggP3[(q >> 6) * FLD + (q & 63)];
     if (tid < DN) {
         rec[DN * DN + tid] = aggy3[tid];
@@ -827,15 +833,16 @@ __global__ void dense_shard_record_kernel(const double* aggP3, const double* agg
         double* t = rec + DN * DN + 2 * DN;
         t[0] = bitsd(red[0]);
         t[1] = bitsd(red[1]);
-        t[2] = __longlong_as_double(0x7ff8000000000000ll);
+        t[2] = step_in ? *step_in : __longlong_as_double(0x7ff8000000000000ll);
         t[3] = (red[3] == ~0ull) ? -1.0 : (double)(long long)red[3];
     }
 }
 
 __global__ void dense_shard_carry_kernel(const double* recs, int rank, double* halo, double* z_out,
-                                         double* dlast, unsigned long long* red) {
+                                         double* dlast, unsigned long long* red, const int* halt) {
     constexpr int R = ODX_SHARD_REC(DN);
     __shared__ double z[DN], t[DN];
+    if (halt && *halt) return;
     const int tid = threadIdx.x;
     if (tid < DN) z[tid] = 0.0;
     __syncthreads();
@@ -857,7 +864,8 @@ __global__ void dense_shard_carry_kernel(const double* recs, int rank, double* h
 
 __global__ void dense_shard_finish_kernel(const double* recs, int rank, const double* dlast,
                                           double* X, long long n, const unsigned long long* red,
-                                          double* step_out) {
+                                          double* step_out, const int* halt) {
+    if (halt && *halt) return;
     const int tid = threadIdx.x;
     const double* xl = recs + (long long)rank * ODX_SHARD_REC(DN) + DN * DN + DN;
     if (tid < DN) X[(n - 1) * DN + tid] = xl[tid] + dlast[tid];
@@ -865,6 +873,65 @@ __global__ void dense_shard_finish_kernel(const double* recs, int rank, const do
 }
 
 size_t dense_shard_workspace(long long n) { return DenseShardLayout(n).total; }
+
+// solve()'s decision for iteration `it` from the gathered records (device-
+// decided protocol; the same reductions and order as sharded.decide): sets
+// *halt (and the pass's stop flag) once the solve has stopped
+__global__ void dense_shard_decide_kernel(const double* recs, int nranks, int it, int max_iters,
+                                          int abort_nonfinite, double rtol, double stol,
+                                          double* hist, double* shist, long long* state,
+                                          int* halt, DenseState* st) {
+    if (threadIdx.x != 0) return;
+    int stop = 0;
+    if (it > 0 && state[0]) {
+        stop = 1;
+    } else {
+        constexpr int R = ODX_SHARD_REC(DN), i_rn = DN * DN + 2 * DN;
+        double rn = 0.0, sc = 0.0, stp = 0.0;
+        unsigned long long bad = ~0ull;
+        for (int q = 0; q < nranks; q++) {
+            const double* r = recs + (long long)q * R;
+            rn = nan_drop_max(rn, r[i_rn]);
+            sc = nan_drop_max(sc, r[i_rn + 1]);
+            stp = nan_drop_max(stp, r[i_rn + 2]);
+            const double b = r[i_rn + 3];
+            if (b >= 0.0 && (unsigned long long)b < bad) bad = (unsigned long long)b;
+        }
+        SolveParams sp;
+        memset(&sp, 0, sizeof(sp));
+        sp.max_iters = max_iters;
+        sp.abort_nonfinite = abort_nonfinite;
+        sp.rtol = rtol;
+        sp.stol = stol;
+        const double step_prev = it > 0 ? stp : __longlong_as_double(0x7ff8000000000000ll);
+        const Decision d = decide(it, sp, rn, bad, step_prev);
+        if (d.status != ODX_ST_SINGULAR) {
+            if (hist) hist[it] = rn;
+            if (shist) shist[it] = sc;
+        }
+        if (d.stop) {
+            state[0] = 1;
+            state[1] = d.status;
+            state[2] = d.iters;
+            state[3] = d.index;
+            stop = 1;
+        } else {
+            state[0] = 0;
+        }
+    }
+    *halt = stop;
+    st->stopped = stop;
+}
+
+// pass reset of the shard's state; a halted solve stays stopped
+__global__ void dense_shard_init_kernel(DenseState* st, unsigned long long* red, const int* halt) {
+    if (threadIdx.x != 0) return;
+    st->stopped = halt ? *halt : 0;
+    st->cur = 0;
+    st->fin = 0;
+    red[0] = red[1] = red[2] = 0ull;
+    red[3] = ~0ull;
+}
 
 static DenseParams dense_shard_params(const DenseShardLayout& lay, char* base, double* X,
                                       long long n) {
@@ -889,7 +956,7 @@ static DenseParams dense_shard_params(const DenseShardLayout& lay, char* base, d
 
 int dense_shard_local(const ProbParams& pp, const StepCoefs& sc, const double* halo,
                       const double* X_local, long long n, long long offset, double* record,
-                      void* ws, size_t ws_bytes, cudaStream_t st) {
+                      void* ws, size_t ws_bytes, cudaStream_t st, bool device_decided) {
     const DenseShardLayout lay(n);
     if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "shard workspace");
     char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
@@ -899,7 +966,10 @@ int dense_shard_local(const ProbParams& pp, const StepCoefs& sc, const double* h
     p.x0 = halo;
     p.offset = offset;
     p.max_iters = 1;
-    dense_init_kernel<<<1, 32, 0, st>>>(p.st, p.red, 1);
+    const int* halt = device_decided ? reinterpret_cast<const int*>(base + lay.halt) : nullptr;
+    const double* step_in =
+        device_decided ? reinterpret_cast<const double*>(base + lay.stepv) : nullptr;
+    dense_shard_init_kernel<<<1, 32, 0, st>>>(p.st, p.red, halt);
     ODX_CUDA(cudaMemsetAsync(p.fcount, 0, 4, st));
     auto kb = dense_band_build_kernel<AllenCahnRows>;
     auto k1 = dense_lu_build_kernel<AllenCahnRows, true>;
@@ -934,14 +1004,16 @@ int dense_shard_local(const ProbParams& pp, const StepCoefs& sc, const double* h
         cnt = q.nchunks;
         b = (b == 1) ? 2 : 1;  // level 1 stays in tP[0]; later levels alternate
     } while (cnt > 1);
-    dense_shard_record_kernel<<<1, 256, 0, st>>>(srcP, srcy, X_local, n, p.red, record);
+    dense_shard_record_kernel<<<1, 256, 0, st>>>(srcP, srcy, X_local, n, p.red, halt, step_in,
+                                                 record);
     ODX_CUDA(cudaGetLastError());
     count_launch(launches + 1);
     return ODX_OK;
 }
 
 int dense_shard_fixup(const double* records, int rank, double* X_local, long long n, double* halo,
-                      double* step_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+                      double* step_out, void* ws, size_t ws_bytes, cudaStream_t st,
+                      bool device_decided) {
     const DenseShardLayout lay(n);
     if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "shard workspace");
     char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
@@ -952,7 +1024,9 @@ int dense_shard_fixup(const double* records, int rank, double* X_local, long lon
     if (int rc = set_smem(dense_fixup_kernel, sizeof(FixSmem))) return rc;
     if (int rc = set_smem(dense_fold_kernel, sizeof(FoldSmem))) return rc;
     if (int rc = set_smem(dense_expand_kernel, sizeof(ExpandSmem))) return rc;
-    dense_shard_carry_kernel<<<1, 64, 0, st>>>(records, rank, halo, z, dlast, p.red);
+    const int* halt = device_decided ? reinterpret_cast<const int*>(base + lay.halt) : nullptr;
+    if (device_decided) step_out = reinterpret_cast<double*>(base + lay.stepv);
+    dense_shard_carry_kernel<<<1, 64, 0, st>>>(records, rank, halo, z, dlast, p.red, halt);
     // group states: fold of the level-1 aggregates from the carry (one CTA, G
     // steps), then every group expands its SHARD_FAN chunk states in parallel
     DenseParams f = p;
@@ -963,10 +1037,33 @@ int dense_shard_fixup(const double* records, int rank, double* X_local, long lon
     dense_fold_kernel<<<1, DTHREADS, sizeof(FoldSmem), st>>>(f);
     dense_expand_kernel<<<lay.G, DTHREADS, sizeof(ExpandSmem), st>>>(p, f.zin);
     dense_fixup_kernel<<<lay.C, DTHREADS, sizeof(FixSmem), st>>>(p, 0);
-    dense_shard_finish_kernel<<<1, 64, 0, st>>>(records, rank, dlast, X_local, n, p.red, step_out);
+    dense_shard_finish_kernel<<<1, 64, 0, st>>>(records, rank, dlast, X_local, n, p.red, step_out,
+                                                halt);
     ODX_CUDA(cudaGetLastError());
     count_launch(6);
     return ODX_OK;
+}
+
+// device-decided step of the d = 64 shard: decision of iteration `it`, then
+// (unless stopped) the fix-up and the next local pass; every kernel after a
+// stop returns at once.  The record's step slot carries this rank's max|dx|.
+int dense_shard_decide_step(const double* records, int rank, int nranks, int it, int max_iters,
+                            int abort_nonfinite, double rtol, double stol, double* hist,
+                            double* shist, long long* state, const ProbParams& pp,
+                            const StepCoefs& sc, double* halo, double* X_local, long long n,
+                            long long offset, double* record, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
+    const DenseShardLayout lay(n);
+    if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "shard workspace");
+    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
+    dense_shard_decide_kernel<<<1, 32, 0, st>>>(
+        records, nranks, it, max_iters, abort_nonfinite, rtol, stol, hist, shist, state,
+        reinterpret_cast<int*>(base + lay.halt), reinterpret_cast<DenseState*>(base + lay.st));
+    ODX_CUDA(cudaGetLastError());
+    count_launch(1);
+    if (int rc = dense_shard_fixup(records, rank, X_local, n, halo, nullptr, ws, ws_bytes, st, true))
+        return rc;
+    return dense_shard_local(pp, sc, halo, X_local, n, offset, record, ws, ws_bytes, st, true);
 }
 
 __global__ void set_i64_dense(long long* q, long long v) { *q = v; }

@@ -200,8 +200,9 @@ def test_emulated_time_sharding_long(oracle, case, mode):
     assert np.abs(X[fin] - ref["X"][fin]).max() <= 1e-9 * scale
 
 
+@pytest.mark.parametrize("mode", ["two_pass", "device"])
 @pytest.mark.parametrize("R", [2, 3])
-def test_emulated_time_sharding_dense(golden_baseline, R):
+def test_emulated_time_sharding_dense(golden_baseline, R, mode):
     """cfg4's d = 64 Allen-Cahn path split along time (two-pass protocol,
     rank aggregate M_r = F_last ... F_first from the chunk aggregates): the
     N = 4096 run converges like the unsharded oracle (golden cfg4s_*)."""
@@ -214,7 +215,7 @@ def test_emulated_time_sharding_dense(golden_baseline, R):
     st = pkg.get_stepper(cfg.stepper, prob)
     guess = np.tile(prob.x0, (n, 1))
     X, res = _emulate(pkg, prob, st, cfg.dt, guess, R, cfg.max_iters, cfg.step_tol,
-                      cfg.abort_nonfinite, "two_pass")
+                      cfg.abort_nonfinite, mode)
     g = golden_baseline
     assert res["status"] == int(g["cfg4s_status"])
     assert abs(res["iters"] - int(g["cfg4s_iters"])) <= 1
@@ -226,7 +227,8 @@ def test_emulated_time_sharding_dense(golden_baseline, R):
     assert (np.abs(h - hr) <= 1e-7 * hr + 1e-9 * hr[0]).all()
 
 
-def test_emulated_time_sharding_dense_full_size():
+@pytest.mark.parametrize("mode", ["two_pass", "device"])
+def test_emulated_time_sharding_dense_full_size(mode):
     """cfg4 at its full N = 65536 over 8 emulated ranks, 3 fixed iterations
     (diverging iterates up to ~1e19): against the unsharded GPU solve, which
     tests/test_gpu_parity.py pins to the oracle."""
@@ -239,7 +241,7 @@ def test_emulated_time_sharding_dense_full_size():
                           tf=n * cfg.dt)
     st = pkg.get_stepper(cfg.stepper, prob)
     guess = np.tile(prob.x0, (n, 1))
-    X, res = _emulate(pkg, prob, st, cfg.dt, guess, 8, 3, 0.0, False, "two_pass")
+    X, res = _emulate(pkg, prob, st, cfg.dt, guess, 8, 3, 0.0, False, mode)
     conf = pkg.NewtonConfig(max_iters=3, abort_on_nonfinite=False)
     ref = solve_batch(prob, st, cfg.dt, prob.x0[None], None, conf)
     R = ref.states[0]

@@ -35,3 +35,19 @@ for it in range(5):
     tl.append(e[0].elapsed_time(e[1])); tf.append(e[1].elapsed_time(e[2]))
 print(f"d=64 R={R} n_local={n}: local {np.median(tl):.3f} ms, fixup {np.median(tf):.3f} ms, "
       f"total {np.median(tl) + np.median(tf):.3f} ms per iteration")
+
+# device-decided step (decision + fix-up + next local), back to back
+from paper_2511_01465_b200 import _native as N  # noqa: E402
+cfgc = N.make_cfg(1000, 0.0, 0.0, False)
+hist = torch.full((1001,), float("nan"), dtype=torch.float64, device="cuda")
+state = torch.zeros(4, dtype=torch.int64, device="cuda")
+sh.recs_dev.copy_(torch.from_numpy(recs))
+sh.decide_step(1, cfgc, hist, hist.clone(), state)
+torch.cuda.synchronize()
+e[0].record()
+for it in range(2, 12):
+    sh.decide_step(it, cfgc, hist, hist.clone(), state)
+e[1].record()
+torch.cuda.synchronize()
+print(f"d=64 R={R} n_local={n}: device-decided step {e[0].elapsed_time(e[1]) / 10:.3f} ms "
+      f"per iteration (back to back), stopped={int(state[0].item())}")
