@@ -200,8 +200,9 @@ int odx_add_inplace(double* X, const double* U, int64_t n, int32_t d, void* stre
  * Rank r owns steps [offset, offset+N_local) of one trajectory; `halo` is the
  * state before its first step (x0 on rank 0, the last state of rank r-1
  * otherwise).  d <= 4 problems run every entry point below; the d = 64
- * Allen-Cahn path (cfg4) runs odx_shard_local, odx_shard_decide_step and
- * odx_shard_fixup (its record carries the 64 x 64 rank aggregate).  Per Newton iteration of the reference loop
+ * Allen-Cahn path (cfg4) runs odx_shard_local, odx_shard_decide_step,
+ * odx_shard_fixup and odx_solve_sharded (its record carries the 64 x 64 rank
+ * aggregate).  Per Newton iteration of the reference loop
  * (newton_pint.py:366-396):
  *   odx_shard_local  builds the local elements (_kernels.py:299-342 /
  *                    :393-464; F is zeroed only at the global step 0), scans

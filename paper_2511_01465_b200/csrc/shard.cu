@@ -356,8 +356,9 @@ int odx_solve_sharded(const odx_problem* P, const odx_stepper* S, const odx_newt
                       double* scaled_hist, int64_t* state, int32_t poll, void* workspace,
                       size_t workspace_bytes, void* stream) {
     using namespace odx;
-    if (!P || !S || P->dim < 1 || P->dim > 4 || dense_supported(P, S))
-        return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4");
+    const bool dense = P && S && dense_supported(P, S);
+    if (!P || !S || ((P->dim < 1 || P->dim > 4) && !dense))
+        return fail(ODX_EUNSUPPORTED, "time sharding supports d <= 4 and the d = 64 Allen-Cahn path");
     if (!C || C->max_iters < 1) return fail(ODX_EINVAL, "max_iters must be >= 1");
     if (!comm) return fail(ODX_EINVAL, "null NCCL communicator");
     if (rank < 0 || rank >= nranks || N_local < 1 || offset < 0)
@@ -390,10 +391,14 @@ int odx_solve_sharded(const odx_problem* P, const odx_stepper* S, const odx_newt
     for (int it = 0; it <= C->max_iters; it++) {
         if (ncclResult_t r = nccl_api().all_gather(rec, recs, (size_t)R, ncclDouble, cm, st))
             return nccl_fail(r, "ncclAllGather");
-        const int rc = with_dim(d, [&]<int D>() {
-            return shard_step_d<D>(P, S, recs, rank, nranks, it, &dec, halo_w, X_local, N_local,
-                                   offset, dt, rec, base, sh, st);
-        });
+        const int rc =
+            dense ? shard_dense_decide_dispatch(P, S, dt, C, recs, rank, nranks, it, halo_w,
+                                                X_local, N_local, offset, rec, hist, scaled_hist,
+                                                reinterpret_cast<long long*>(state), base, sh, st)
+                  : with_dim(d, [&]<int D>() {
+                        return shard_step_d<D>(P, S, recs, rank, nranks, it, &dec, halo_w,
+                                               X_local, N_local, offset, dt, rec, base, sh, st);
+                    });
         if (rc) return rc;
         if (poll > 0 && it < C->max_iters && (it + 1) % poll == 0) {
             long long stopped = 0;  // identical on every rank: all leave together

@@ -334,8 +334,8 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
     import torch.distributed as dist
     if protocol not in ("device", "native", "host", "two_pass"):
         raise ValueError(f"unknown protocol {protocol!r}")
-    if problem.dim > 4 and protocol in ("native", "host"):
-        protocol = "device"  # the d = 64 shard: device-decided or two-pass protocols
+    if problem.dim > 4 and protocol == "host":
+        protocol = "device"  # the d = 64 shard has no host-decided fused step
     R = dist.get_world_size(group)
     r = dist.get_rank(group)
     d = problem.dim

@@ -133,15 +133,18 @@ def test_nccl_drivers_world_size_one(oracle):
         c4 = CONFIGS[4]
         ac = pkg.allen_cahn(n=c4.dim, eps=c4.params[0], dx=c4.params[1], u0=c4.x0s()[0],
                             tf=4096 * c4.dt)
-        Xa = torch.from_numpy(np.tile(ac.x0, (4096, 1))).cuda()
-        rep = solve_time_sharded(ac, pkg.get_stepper(c4.stepper, ac), c4.dt, Xa, 0,
-                                 pkg.NewtonConfig(max_iters=c4.max_iters, step_tol=c4.step_tol))
         import numpy as _np
         g = _np.load(Path(__file__).resolve().parent / "golden" / "baseline.npz")
-        assert rep.status == int(g["cfg4s_status"])
-        assert abs(rep.iterations_run - int(g["cfg4s_iters"])) <= 1
         ref = g["cfg4s_X_sub"]
-        assert _np.abs(Xa.cpu().numpy()[::32] - ref).max() <= 1e-9 * max(1.0, float(_np.abs(ref).max()))
+        for protocol in ("device", "native", "two_pass"):
+            Xa = torch.from_numpy(np.tile(ac.x0, (4096, 1))).cuda()
+            rep = solve_time_sharded(ac, pkg.get_stepper(c4.stepper, ac), c4.dt, Xa, 0,
+                                     pkg.NewtonConfig(max_iters=c4.max_iters,
+                                                      step_tol=c4.step_tol), protocol=protocol)
+            assert rep.status == int(g["cfg4s_status"]), protocol
+            assert abs(rep.iterations_run - int(g["cfg4s_iters"])) <= 1, protocol
+            err = _np.abs(Xa.cpu().numpy()[::32] - ref).max()
+            assert err <= 1e-9 * max(1.0, float(_np.abs(ref).max())), protocol
         cfg = CONFIGS[3]
         lor = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=cfg.n_steps * cfg.dt)
         local, off, gathered = solve_batch_sharded(lor, pkg.get_stepper("rk4", lor), cfg.dt,
