@@ -253,3 +253,40 @@ def test_emulated_time_sharding_dense_full_size(mode):
     scale = max(1.0, float(np.abs(R[fin]).max()))
     assert np.abs(X[fin] - R[fin]).max() <= 1e-9 * scale
     assert res["iters"] == int(ref.iterations_run[0]) and res["status"] == int(ref.status[0])
+
+
+@pytest.mark.parametrize("mode", ["two_pass", "host", "device"])
+@pytest.mark.parametrize("n,R", [(5, 5), (7, 3), (2, 2), (1000, 7)])
+def test_emulated_time_sharding_tiny_ranks(oracle, n, R, mode):
+    """Ranks with one or a few steps (a single partial tile and chunk)."""
+    import paper_2511_01465_b200 as pkg
+    dt = 1e-2
+    prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
+    st = pkg.get_stepper("rk4", prob)
+    guess = np.tile(prob.x0, (n, 1))
+    X, res = _emulate(pkg, prob, st, dt, guess, R, 4, 0.0, False, mode)
+    ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), prob.x0, guess, dt, 4,
+                       abort_nonfinite=False)
+    assert res["status"] == ref["status"] and res["iters"] == ref["iters"]
+    fin = np.isfinite(ref["X"]).all(axis=1)
+    assert np.array_equal(fin, np.isfinite(X).all(axis=1))
+    scale = max(1.0, float(np.abs(ref["X"][fin]).max()))
+    assert np.abs(X[fin] - ref["X"][fin]).max() <= 1e-9 * scale
+
+
+@pytest.mark.parametrize("mode", ["two_pass", "device"])
+def test_emulated_time_sharding_dense_tiny_ranks(golden_baseline, mode):
+    """d = 64 ranks of 2 steps (one chunk, a one-level tree)."""
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200.configs import CONFIGS
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    cfg = CONFIGS[4]
+    n = 8
+    prob = pkg.allen_cahn(n=cfg.dim, eps=cfg.params[0], dx=cfg.params[1], u0=cfg.x0s()[0],
+                          tf=n * cfg.dt)
+    st = pkg.get_stepper(cfg.stepper, prob)
+    X, res = _emulate(pkg, prob, st, cfg.dt, np.tile(prob.x0, (n, 1)), 4, 3, 0.0, False, mode)
+    ref = solve_batch(prob, st, cfg.dt, prob.x0[None], None,
+                      pkg.NewtonConfig(max_iters=3, abort_on_nonfinite=False))
+    R = ref.states[0]
+    assert np.abs(X - R).max() <= 1e-9 * max(1.0, float(np.abs(R).max()))
