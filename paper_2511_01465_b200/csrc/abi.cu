@@ -281,9 +281,14 @@ static int solve_each(const odx_problem* P, const odx_stepper* S, SolveParams& p
 static int solve_impl(const odx_problem* P, const odx_stepper* S, SolveParams& p, void* ws,
                       size_t ws_bytes, cudaStream_t st, bool query, size_t* need) {
     const bool long_traj = dense_supported(P, S) || p.N > resident_max_steps(P->dim);
-    const bool misaligned = !query && (reinterpret_cast<uintptr_t>(p.X) & 15) != 0;
-    if (long_traj && (p.B > 1 || misaligned))
-        return solve_each(P, S, p, ws, ws_bytes, st, query, need);
+    if (long_traj && p.B > 1) return solve_each(P, S, p, ws, ws_bytes, st, query, need);
+    if (long_traj && !query && (reinterpret_cast<uintptr_t>(p.X) & 15) != 0) {
+        // one misaligned trajectory: staged when the workspace has room for the
+        // copy (a B > 1 query's size), else the kernels report the alignment
+        size_t each = 0;
+        if (solve_each(P, S, p, nullptr, 0, st, true, &each) == ODX_OK && ws_bytes >= each)
+            return solve_each(P, S, p, ws, ws_bytes, st, false, nullptr);
+    }
     if (dense_supported(P, S)) return dense_solve(P, S, p, ws, ws_bytes, st, query, need);
     int rc = with_small_problem(P->problem_id, P->dim, SolveFn{S, &p, ws, ws_bytes, st, query, need});
     if (rc == ODX_EUNSUPPORTED && odx_last_error()[0] == 0)
