@@ -24,17 +24,19 @@
 namespace odx {
 
 // contiguous chunks per rank = CTAs of the build / apply / fused kernels (each
-// CTA walks its chunk's tiles in order): three per SM, the fused kernel's
+// CTA walks its chunk's tiles in order): two per SM, the fused kernel's
 // residency for d <= 2
-inline int shard_chunks() { return 3 * num_sms(); }
+inline int shard_chunks() { return 2 * num_sms(); }
 
 // tile shape of the shard kernels: 128 threads x ITEMS consecutive steps each.
 // ITEMS is odd for d <= 2 so a lane's items (ITEMS*E doubles apart in shared
-// memory) fall on distinct bank pairs up to 2-way; 3 items also leave room
-// for three CTAs per SM in the fused kernel's shared memory.
+// memory) fall on distinct bank pairs up to 2-way.  Measured for d = 2 (cfg5):
+// 5 items (640-step tiles, two CTAs per SM at 253 registers, five builds
+// interleaved) 1.678 ms per iteration; 3 items (three CTAs per SM at 168
+// registers) 1.703 ms; 4 items 16-way bank conflicts.
 constexpr int SHARD_THREADS = 128;
 template <int D>
-constexpr int shard_items() { return D <= 2 ? 3 : 2; }
+constexpr int shard_items() { return D <= 2 ? 5 : 2; }
 
 template <int D>
 struct ShardTiledLayout {
@@ -297,7 +299,7 @@ struct ShardFusedSmem {
 // staged in smem, written over the old ones, and folded into the chunk
 // aggregate; rn / sc / first singular step / max|dx| -> red.
 template <class P, int KIND, int S, int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS, 3) shard_fused_kernel(const ShardFusedParams fp) {
+__global__ void __launch_bounds__(THREADS, ITEMS <= 3 ? 3 : 2) shard_fused_kernel(const ShardFusedParams fp) {
     constexpr int D = P::D, E = D * D + D, NW = THREADS / 32, T = THREADS * ITEMS;
     using SM = ShardFusedSmem<D, THREADS, ITEMS>;
     extern __shared__ __align__(16) unsigned char fused_raw[];
