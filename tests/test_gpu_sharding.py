@@ -163,6 +163,7 @@ def test_nccl_drivers_world_size_one(oracle):
     ("vdp_long", "rk4", 1 << 20, 1e-3, 2, 4),
     ("lorenz_be", "backward_euler", 300000, 1e-5, 3, 5),
     ("linear4_rk4", "rk4", 700001, 1e-4, 3, 3),
+    ("logistic_be", "backward_euler", 500003, 1e-5, 4, 4),
 ])
 def test_emulated_time_sharding_long(oracle, case, mode):
     import paper_2511_01465_b200 as pkg
@@ -171,6 +172,8 @@ def test_emulated_time_sharding_long(oracle, case, mode):
         prob = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt)
     elif name == "lorenz_be":
         prob = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=n * dt)
+    elif name == "logistic_be":
+        prob = pkg.problems.logistic(tf=n * dt)
     else:
         A = np.array([[-1.0, 0.5, 0.0, 0.1], [0.0, -2.0, 0.3, 0.0],
                       [0.2, 0.0, -0.5, 0.4], [0.0, -0.1, 0.0, -1.5]])
