@@ -214,7 +214,29 @@ def _resolve_guess(guess, problem: OdeProblem, n: int, dt: float) -> Trajectory:
     return initial_guess(guess, problem, n)
 
 
+_NATIVE_CACHE: dict = {}
+
+
 def _validate(problem: OdeProblem, stepper: StepperIncrement):
+    # (problem, stepper) are frozen dataclasses: their descriptors and the
+    # device-path check are cached per object pair (weakly: a recycled id()
+    # is detected), ~4 us per call on the end-to-end path
+    key = (id(problem), id(stepper))
+    hit = _NATIVE_CACHE.get(key)
+    if hit is not None and hit[0]() is problem and hit[1]() is stepper:
+        return hit[2], hit[3]
+    P, S = _validate_uncached(problem, stepper)
+    import weakref
+    if len(_NATIVE_CACHE) > 256:  # many short-lived problems: keep the cache small
+        _NATIVE_CACHE.clear()
+    try:
+        _NATIVE_CACHE[key] = (weakref.ref(problem), weakref.ref(stepper), P, S)
+    except TypeError:
+        pass
+    return P, S
+
+
+def _validate_uncached(problem: OdeProblem, stepper: StepperIncrement):
     if stepper.problem is not problem:
         raise ValueError("stepper was built for a different problem instance")
     if problem.device is None:
@@ -228,10 +250,17 @@ def _validate(problem: OdeProblem, stepper: StepperIncrement):
     return P, S
 
 
+_DEVICES: dict = {}
+
+
 def _device(device):
     import torch
     if device is None:
-        device = torch.device("cuda", torch.cuda.current_device())
+        idx = torch.cuda.current_device()
+        dev = _DEVICES.get(idx)
+        if dev is None:
+            dev = _DEVICES[idx] = torch.device("cuda", idx)
+        return dev
     device = torch.device(device)
     if device.type != "cuda":
         raise ValueError("the B200 solver runs on CUDA devices only")
