@@ -479,7 +479,7 @@ def main():
         stop_rule = None
     else:
         # e2e through the public API with host buffers
-        e2e_durs, h2d, d2h = e2e_steps(w, max(3, args.steps // 2), 2)
+        e2e_durs, h2d, d2h = e2e_steps(w, max(5, args.steps), max(3, args.warmup))
         e2e_ms = reduce_max(sum(e2e_durs), world) / len(e2e_durs)
         e2e_val = units_per_step / (e2e_ms * 1e-3)
         # BASELINE stop-rule solve of the same config
