@@ -26,6 +26,7 @@
 #include <cstdint>
 
 #include "scan.cuh"
+#include "sm100.cuh"
 
 namespace odx {
 
@@ -409,13 +410,14 @@ grid_resident_kernel(const GridResParams gp) {
     __shared__ int s_whas[NW];
 
     const SolveParams& p = gp.sp;
-    // CTA g's last row for CTA g+1: values first, then the tag with release
-    // semantics; the reader acquires the tag before reading the values (a
-    // 16-byte {value, tag} access is not single-copy atomic: a torn read can
-    // pair the new tag with the previous iterate's value)
+    // CTA g's last row for CTA g+1: one 16-byte {value, tag} chunk per
+    // component (st_chunk / ld_chunk: a single aligned transaction, as the
+    // streaming kernel's look-back records), so the reader validates every
+    // value by its own tag and the writer needs no release fence — a fence
+    // here stalled the writing thread, and with it the next iteration's
+    // entry barrier, by an L2 round trip
     struct alignas(64) HaloRow {
-        unsigned long long tag;
-        double v[4];
+        Chunk c[4];
     };
     HaloRow* halos = reinterpret_cast<HaloRow*>(gp.halos);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -451,20 +453,20 @@ grid_resident_kernel(const GridResParams gp) {
             if (i == 0 && tid == 0 && it > 0 && g > 0) {
                 const HaloRow* src = halos + (g - 1);
                 const unsigned long long want = (unsigned long long)it;
-                unsigned long long tag;
+                Chunk ch[D];
                 int spins = 0;
                 while (true) {
-                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];"
-                                 : "=l"(tag) : "l"(&src->tag) : "memory");
-                    if (tag == want) break;
+                    bool ok = true;
+#pragma unroll
+                    for (int k = 0; k < D; k++) {
+                        ch[k] = ld_chunk(&src->c[k]);
+                        ok = ok && ch[k].tag == want;
+                    }
+                    if (ok) break;
                     if (++spins > 8) __nanosleep(20);
                 }
 #pragma unroll
-                for (int k = 0; k < D; k++) {
-                    double v;
-                    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(&src->v[k]) : "memory");
-                    sm.xs[L::idx(k)] = v;
-                }
+                for (int k = 0; k < D; k++) sm.xs[L::idx(k)] = ch[k].v;
             }
             E::build_item(prob, p.sc, sm, base, N, i, el[i], rn, scn, bad);
         }
@@ -598,13 +600,8 @@ grid_resident_kernel(const GridResParams gp) {
         if (g + 1 < G && tid == (int)((rows - 1) / ITEMS)) {
             HaloRow* dst = halos + g;
 #pragma unroll
-            for (int k = 0; k < D; k++) {
-                const double v = sm.xs[L::idx((int)rows * D + k)];
-                asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(&dst->v[k]), "d"(v) : "memory");
-            }
-            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&dst->tag),
-                         "l"((unsigned long long)(it + 1))
-                         : "memory");
+            for (int k = 0; k < D; k++)
+                st_chunk(&dst->c[k], sm.xs[L::idx((int)rows * D + k)], (unsigned long long)(it + 1));
         }
         // max|dx|: warp maxima now; the block max and its atomic ride on the
         // next iteration's reduction (before that iteration's barrier)

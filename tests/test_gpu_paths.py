@@ -96,3 +96,27 @@ def test_fused_tiled_deterministic():
     b = solve_batch(prob, st, dt, prob.x0[None], guess, conf)
     assert np.array_equal(a.states, b.states, equal_nan=True)
     assert np.array_equal(a.residual_history, b.residual_history, equal_nan=True)
+
+
+def test_grid_resident_deterministic():
+    """cfg2's grid-resident solve (halo rows handed over as tagged 16-byte
+    chunks, aggregates double-buffered by iteration parity) repeated: every
+    run bit-identical."""
+    import torch
+    import paper_2511_01465_b200 as pkg
+    from paper_2511_01465_b200.newton_pint import solve_device
+    n = 65536
+    prob = pkg.van_der_pol(mu=10.0, x0=(2.0, 0.0), tf=n * 1e-3)
+    st = pkg.get_stepper("backward_euler", prob)
+    P, S = prob.native(), st.native()
+    x0 = torch.tensor([[2.0, 0.0]], dtype=torch.float64, device="cuda")
+    X0 = x0[:, None, :].expand(1, n, 2).contiguous()
+    conf = pkg.NewtonConfig(max_iters=10, abort_on_nonfinite=False)
+    ref = None
+    for _ in range(60):
+        X = X0.clone()
+        solve_device(P, S, x0, X, 1e-3, conf)
+        if ref is None:
+            ref = X
+        else:
+            assert torch.equal(torch.nan_to_num(X, nan=7.0), torch.nan_to_num(ref, nan=7.0))
