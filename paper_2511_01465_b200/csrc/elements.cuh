@@ -407,6 +407,87 @@ __device__ __forceinline__ bool build_implicit_step(const P& prob, const StepCoe
     return false;
 }
 
+// Branch-free form of lu_factor_reg + build_implicit_step (same arithmetic
+// for every non-singular block; a singular block still yields F = c = 0 and
+// true): no early exits, so two items' builds written back to back can be
+// interleaved by the compiler (the grid-resident kernel's latency-bound build).
+template <int D>
+__device__ __forceinline__ int lu_factor_reg_bf(double* A, int* piv, double* rinv) {
+    int st = -1;
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+        int p = k;
+        double best = fabs(A[k * D + k]);
+#pragma unroll
+        for (int i = k + 1; i < D; i++) {
+            double v = fabs(A[i * D + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        if (best < 1e-300 && st < 0) st = k;
+        piv[k] = p;
+#pragma unroll
+        for (int i = k + 1; i < D; i++) {
+            if (p == i) {
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    double t = A[k * D + j];
+                    A[k * D + j] = A[i * D + j];
+                    A[i * D + j] = t;
+                }
+            }
+        }
+        const double inv = div_rn(1.0, A[k * D + k]);
+        rinv[k] = inv;
+#pragma unroll
+        for (int i = k + 1; i < D; i++) {
+            double m = A[i * D + k] * inv;
+            A[i * D + k] = m;
+#pragma unroll
+            for (int j = k + 1; j < D; j++) A[i * D + j] = __dsub_rn(A[i * D + j], __dmul_rn(m, A[k * D + j]));
+        }
+    }
+    return st;
+}
+
+template <class P>
+__device__ __forceinline__ bool build_implicit_step_bf(const P& prob, const StepCoefs& sc,
+                                                      const double* prev, const double* xk,
+                                                      bool first, Elem<P::D>& el, double* h) {
+    constexpr int D = P::D;
+    double fprev[D], fnext[D], Jp[D * D], A[D * D];
+    prob.f(prev, fprev);
+    prob.f(xk, fnext);
+    prob.jac(prev, Jp);
+    prob.jac(xk, A);
+#pragma unroll
+    for (int r = 0; r < D; r++)
+        h[r] = xk[r] - prev[r] - sc.dt * (sc.w_prev * fprev[r] + sc.w_next * fnext[r]);
+#pragma unroll
+    for (int r = 0; r < D; r++)
+#pragma unroll
+        for (int c = 0; c < D; c++)
+            A[r * D + c] = __dsub_rn((r == c) ? 1.0 : 0.0, __dmul_rn(sc.dt_wnext, A[r * D + c]));
+    int piv[D];
+    double rinv[D];
+    const bool sing = lu_factor_reg_bf<D>(A, piv, rinv) >= 0;
+    double col[D];
+#pragma unroll
+    for (int r = 0; r < D; r++) col[r] = -h[r];
+    lu_solve_reg<D>(A, piv, rinv, col);
+#pragma unroll
+    for (int r = 0; r < D; r++) el.c[r] = sing ? 0.0 : col[r];
+#pragma unroll
+    for (int c = 0; c < D; c++) {
+#pragma unroll
+        for (int r = 0; r < D; r++)
+            col[r] = __dadd_rn(__dmul_rn(sc.dt_wprev, Jp[r * D + c]), (r == c) ? 1.0 : 0.0);
+        lu_solve_reg<D>(A, piv, rinv, col);
+#pragma unroll
+        for (int r = 0; r < D; r++) el.F[r * D + c] = (sing || first) ? 0.0 : col[r];
+    }
+    return sing;
+}
+
 // Uniform entry used by the fused kernels: KIND 0 = explicit RK with S stages,
 // KIND 1 = implicit weighted.  Returns true for a singular implicit block.
 template <class P, int KIND, int S>

@@ -162,6 +162,30 @@ struct SmallEngine {
         }
     }
 
+    // build_item for an item known to exist, branch-free for implicit steps
+    // (two calls written back to back interleave)
+    __device__ __forceinline__ static void build_item_bf(const P& prob, const StepCoefs& sc,
+                                                         const Shared& sm, long long base, int i,
+                                                         Elem<D>& el, double& rn, double& scn,
+                                                         unsigned long long& bad) {
+        const int r = threadIdx.x * ITEMS + i;
+        const long long k = base + r;
+        double prev[D], xk[D], h[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            prev[j] = sm.xs[L::idx(r * D + j)];
+            xk[j] = sm.xs[L::idx((r + 1) * D + j)];
+        }
+        bool sing;
+        if constexpr (KIND == 1)
+            sing = build_implicit_step_bf<P>(prob, sc, prev, xk, k == 0, el, h);
+        else
+            sing = build_step<P, KIND, S>(prob, sc, prev, xk, k == 0, el, h);
+        rn = nan_drop_max(rn, row_max_abs<D>(h));
+        if (KIND == 1) scn = nan_drop_max(scn, row_max_abs<D>(el.c));
+        if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
+    }
+
     // Fold this thread's items, scan the block, and leave the warp totals in
     // shared memory.  Returns the thread inclusive aggregate (within its warp).
     __device__ __forceinline__ static void block_scan(Shared& sm, long long base, long long N,
@@ -447,10 +471,8 @@ grid_resident_kernel(const GridResParams gp) {
         // items in the order 1..ITEMS-1, 0: thread 0's item 0 needs the halo
         // from CTA g-1 (its last row of the current iterate), whose arrival
         // then overlaps the thread's other items
-#pragma unroll
-        for (int ii = 0; ii < ITEMS; ii++) {
-            const int i = (ii + 1) % ITEMS;
-            if (i == 0 && tid == 0 && it > 0 && g > 0) {
+        auto fetch_halo = [&]() {
+            if (tid == 0 && it > 0 && g > 0) {
                 const HaloRow* src = halos + (g - 1);
                 const unsigned long long want = (unsigned long long)it;
                 Chunk ch[D];
@@ -468,7 +490,25 @@ grid_resident_kernel(const GridResParams gp) {
 #pragma unroll
                 for (int k = 0; k < D; k++) sm.xs[L::idx(k)] = ch[k].v;
             }
-            E::build_item(prob, p.sc, sm, base, N, i, el[i], rn, scn, bad);
+        };
+        if (KIND == 1 && ITEMS % 2 == 0 && rows == T) {
+            // implicit, full tile: pairs (1,2), (3,4), ..., (ITEMS-1, 0) built
+            // back to back (branch-free: they interleave); the halo before the
+            // pair that holds item 0
+#pragma unroll
+            for (int ii = 1; ii < ITEMS; ii += 2) {
+                const int i0 = ii, i1 = (ii + 1) % ITEMS;
+                if (i1 == 0) fetch_halo();
+                E::build_item_bf(prob, p.sc, sm, base, i0, el[i0], rn, scn, bad);
+                E::build_item_bf(prob, p.sc, sm, base, i1, el[i1], rn, scn, bad);
+            }
+        } else {
+#pragma unroll
+            for (int ii = 0; ii < ITEMS; ii++) {
+                const int i = (ii + 1) % ITEMS;
+                if (i == 0) fetch_halo();
+                E::build_item(prob, p.sc, sm, base, N, i, el[i], rn, scn, bad);
+            }
         }
         GR_STAMP(2);
         Elem<D> agg;
