@@ -491,8 +491,8 @@ grid_resident_kernel(const GridResParams gp) {
                 for (int k = 0; k < D; k++) sm.xs[L::idx(k)] = ch[k].v;
             }
         };
-        if (KIND == 1 && ITEMS % 2 == 0 && rows == T) {
-            // implicit, full tile: pairs (1,2), (3,4), ..., (ITEMS-1, 0) built
+        if (ITEMS % 2 == 0 && rows == T) {
+            // full tile: pairs (1,2), (3,4), ..., (ITEMS-1, 0) built
             // back to back (branch-free: they interleave); the halo before the
             // pair that holds item 0
 #pragma unroll
