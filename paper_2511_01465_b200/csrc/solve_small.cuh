@@ -315,7 +315,15 @@ resident_solve_kernel(const SolveParams p) {
         Elem<D> el[ITEMS];
         double rn = 0.0, scn = 0.0;
         unsigned long long bad = ~0ull;
-        E::build_items(prob, p.sc, sm, 0, N, el, rn, scn, bad);
+        if (ITEMS % 2 == 0 && N == E::T) {  // full tile: items in interleavable pairs
+#pragma unroll
+            for (int i = 0; i < ITEMS; i += 2) {
+                E::build_item_bf(prob, p.sc, sm, 0, i, el[i], rn, scn, bad);
+                E::build_item_bf(prob, p.sc, sm, 0, i + 1, el[i + 1], rn, scn, bad);
+            }
+        } else {
+            E::build_items(prob, p.sc, sm, 0, N, el, rn, scn, bad);
+        }
         rn = warp_max_nan_drop(rn);
         scn = warp_max_nan_drop(scn);
         bad = warp_min_u64(bad);
