@@ -186,6 +186,33 @@ struct SmallEngine {
         if (sing && (unsigned long long)k < bad) bad = (unsigned long long)k;
     }
 
+    // NI consecutive explicit items (i0 .. i0+NI-1, all present) built
+    // stage-interleaved (build_explicit_multi)
+    template <int NI>
+    __device__ __forceinline__ static void build_items_multi(const P& prob, const StepCoefs& sc,
+                                                             const Shared& sm, long long base,
+                                                             int i0, Elem<D>* el, double& rn) {
+        double prev[NI][D], xk[NI][D], h[NI][D];
+        bool first[NI];
+        Elem<D> e[NI];
+#pragma unroll
+        for (int n = 0; n < NI; n++) {
+            const int r = threadIdx.x * ITEMS + i0 + n;
+#pragma unroll
+            for (int j = 0; j < D; j++) {
+                prev[n][j] = sm.xs[L::idx(r * D + j)];
+                xk[n][j] = sm.xs[L::idx((r + 1) * D + j)];
+            }
+            first[n] = (base + r == 0);
+        }
+        build_explicit_multi<P, S, NI>(prob, sc, prev, xk, first, e, h);
+#pragma unroll
+        for (int n = 0; n < NI; n++) {
+            el[n] = e[n];
+            rn = nan_drop_max(rn, row_max_abs<D>(h[n]));
+        }
+    }
+
     // Fold this thread's items, scan the block, and leave the warp totals in
     // shared memory.  Returns the thread inclusive aggregate (within its warp).
     __device__ __forceinline__ static void block_scan(Shared& sm, long long base, long long N,
@@ -315,7 +342,10 @@ resident_solve_kernel(const SolveParams p) {
         Elem<D> el[ITEMS];
         double rn = 0.0, scn = 0.0;
         unsigned long long bad = ~0ull;
-        if (ITEMS % 2 == 0 && N == E::T) {  // full tile: items in interleavable pairs
+        if (KIND == 0 && ITEMS % 2 == 0 && N == E::T) {  // explicit, full tile: stage-interleaved pairs
+#pragma unroll
+            for (int i = 0; i < ITEMS; i += 2) E::template build_items_multi<2>(prob, p.sc, sm, 0, i, &el[i], rn);
+        } else if (ITEMS % 2 == 0 && N == E::T) {  // full tile: items in interleavable pairs
 #pragma unroll
             for (int i = 0; i < ITEMS; i += 2) {
                 E::build_item_bf(prob, p.sc, sm, 0, i, el[i], rn, scn, bad);
