@@ -505,6 +505,19 @@ __global__ void __launch_bounds__(THREADS, ITEMS <= 3 ? 3 : 2) shard_fused_kerne
             build_explicit_multi<P, S, ITEMS>(prob, fp.sc, prev, xn, first, e, h);
 #pragma unroll
             for (int q = 0; q < ITEMS; q++) take(q, kb + q, e[q], h[q], false);
+        } else if (KIND == 1 && kb + ITEMS <= N) {
+            // implicit, all items present: branch-free builds back to back
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) {
+                const long long k = kb + q;
+                double prev[D], h[D];
+#pragma unroll
+                for (int j = 0; j < D; j++) prev[j] = (q == 0) ? p0[j] : xn[q - 1][j];
+                Elem<D> e;
+                const bool sing =
+                    build_implicit_step_bf<P>(prob, fp.sc, prev, xn[q], fp.offset + k == 0, e, h);
+                take(q, k, e, h, sing);
+            }
         } else {
 #pragma unroll
             for (int q = 0; q < ITEMS; q++) {

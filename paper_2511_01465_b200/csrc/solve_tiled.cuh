@@ -129,6 +129,22 @@ tiled_build_kernel(const TiledParams tp, int it) {
             build_explicit_multi<P, S, ITEMS>(prob, p.sc, prev, xk, first, e, h);
 #pragma unroll
             for (int q = 0; q < ITEMS; q++) take(q, kb + q, e[q], h[q], false);
+        } else if (KIND == 1 && kb + ITEMS <= N) {
+            // implicit, all items present: branch-free builds back to back
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) {
+                const long long k = kb + q;
+                double prev[D], xk[D], h[D];
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    prev[j] = (k == 0) ? tp.halo[j] : p.X[(k - 1) * D + j];
+                    xk[j] = p.X[k * D + j];
+                }
+                Elem<D> e;
+                const bool sing =
+                    build_implicit_step_bf<P>(prob, p.sc, prev, xk, tp.offset + k == 0, e, h);
+                take(q, k, e, h, sing);
+            }
         } else {
 #pragma unroll
             for (int q = 0; q < ITEMS; q++) {
