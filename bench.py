@@ -271,6 +271,14 @@ class TimeShardedWorkload:
         return (np.array([r.iterations_run]), np.array([r.status]), np.array([r.status_index]))
 
 
+# the device path each BASELINE config runs (kernel table)
+ROUTE = {1: "resident_solve_kernel (one CTA, 256 threads x 4 steps)",
+         2: "grid_resident_kernel (128 co-resident CTAs x 512 steps)",
+         3: "resident_solve_kernel (one CTA per trajectory, 256 x 8)",
+         4: "dense_band/lu_build + dense_agg (DMMA) + dense_fold + dense_fixup",
+         5: "tiled_build + per iteration shard_step_carry / shard_fused / shard_scan_record"}
+
+
 def flush_l2(buf):
     buf.add_(1.0)  # 256 MB written > 126 MB L2
 
@@ -514,6 +522,7 @@ def main():
                 oi, os_, ox = ow.outcome()
                 extra[ow.cfg.name] = {
                     "fixed_iters": args.iters, "ms": round(oms, 4), "newton_steps_per_s": ov,
+                    "path": ROUTE.get(ocid),
                     "roofline": roofline_for(ocid, ow.n, ow.B, args.iters, oms, hbm, hbm_src,
                                              fp64, fp64_src),
                     "stop_rule": {"ms": round(statistics.median(sd), 4),
@@ -572,6 +581,7 @@ def main():
                        "newton_iters": args.iters,
                        "mode": "fixed iterations, non-aborting (SURVEY 8d)",
                        "l2": "flushed between steps (256 MB write)",
+                       "path": ROUTE.get(cid),
                        "parallelism": ("single GPU" if world == 1 else
                                        f"time-sharded x{world}" if sharded_time else
                                        f"batch-sharded x{world}" if cid == 3 else
