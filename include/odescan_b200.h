@@ -149,6 +149,13 @@ int odx_solve_host(const odx_problem* P, const odx_stepper* S,
                    double* hist, double* scaled_hist,
                    int32_t* iters, int32_t* status, int64_t* status_index, void* stream);
 
+/* Host staging-copy threads of odx_solve_host — the counterpart of
+ * odescan.threads (threads.py:17-32: max_threads / set_threads).  The pool is
+ * sized once (ODX_HOST_THREADS, default min(8, cores/2)); set clamps n into
+ * [1, max] and returns the count now used.                                  */
+int odx_host_threads_max(void);
+int odx_set_host_threads(int n);
+
 /* The starting iterate built on the device (newton_pint.initial_guess
  * :174-207): X (B x N x d, device) from x0 (B x d, device) by an
  * ODX_GUESS_* policy; dt = (tf - t0) / N as the reference computes it

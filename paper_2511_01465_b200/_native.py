@@ -28,7 +28,8 @@ PROB_LINEAR = 10
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = (
     "odx_abi_version", "odx_last_error", "odx_supported", "odx_launch_count", "odx_solve_workspace_bytes",
-    "odx_solve", "odx_solve_host", "odx_initial_guess", "odx_seq_march", "odx_parareal_coarse", "odx_build_explicit", "odx_build_implicit",
+    "odx_solve", "odx_solve_host", "odx_host_threads_max", "odx_set_host_threads",
+    "odx_initial_guess", "odx_seq_march", "odx_parareal_coarse", "odx_build_explicit", "odx_build_implicit",
     "odx_scan_affine_workspace_bytes", "odx_scan_affine", "odx_max_abs", "odx_add_inplace",
     "odx_shard_workspace_bytes", "odx_shard_local", "odx_shard_fixup", "odx_shard_step",
     "odx_shard_decide_step", "odx_nccl_available", "odx_nccl_unique_id", "odx_nccl_comm_init",
@@ -77,6 +78,10 @@ def lib():
     L.odx_last_error.restype = C.c_char_p
     L.odx_launch_count.restype = C.c_int64
     L.odx_supported.restype = C.c_int
+    L.odx_host_threads_max.restype = C.c_int
+    L.odx_host_threads_max.argtypes = []
+    L.odx_set_host_threads.restype = C.c_int
+    L.odx_set_host_threads.argtypes = [C.c_int]
     L.odx_supported.argtypes = [P_, S_]
     L.odx_solve_workspace_bytes.restype = sz
     L.odx_solve_workspace_bytes.argtypes = [P_, S_, i64, i64, CFG]

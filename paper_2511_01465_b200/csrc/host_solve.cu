@@ -112,7 +112,9 @@ class CopyPool {
     }
     void copy(void* dst, const void* src, size_t n) {
         // a forked child has no worker threads (fork copies only the caller)
-        const int T = forked_.load(std::memory_order_relaxed) ? 0 : (int)workers_.size();
+        int T = forked_.load(std::memory_order_relaxed) ? 0 : (int)workers_.size();
+        const int act = active_.load(std::memory_order_relaxed) - 1;  // the caller copies too
+        if (act < T) T = act < 0 ? 0 : act;
         if (T == 0 || n < (size_t(1) << 18)) {
             nt_copy(static_cast<char*>(dst), static_cast<const char*>(src), n);
             return;
@@ -123,6 +125,7 @@ class CopyPool {
         src_ = static_cast<const char*>(src);
         n_ = n;
         chunk_ = chunk;
+        used_ = T;
         pending_.store(T, std::memory_order_relaxed);
         gen_.fetch_add(1, std::memory_order_seq_cst);  // publishes the job (release)
         if (sleepers_.load(std::memory_order_seq_cst) > 0) {
@@ -132,6 +135,15 @@ class CopyPool {
         const size_t lo = (size_t)T * chunk;  // the caller copies the last part
         if (lo < n) nt_copy(dst_ + lo, src_ + lo, n - lo);
         while (pending_.load(std::memory_order_acquire) != 0) _mm_pause();
+    }
+
+    // threads.max_threads / set_threads (threads.py:17-32): the pool size is
+    // fixed at first use; set_threads clamps into [1, max] and returns it
+    int max_threads() const { return (int)workers_.size() + 1; }
+    int set_threads(int n) {
+        const int used = n < 1 ? 1 : (n > max_threads() ? max_threads() : n);
+        active_.store(used, std::memory_order_relaxed);
+        return used;
     }
 
   private:
@@ -159,6 +171,7 @@ class CopyPool {
                 sleepers_.fetch_sub(1, std::memory_order_relaxed);
             }
             seen = gen_.load(std::memory_order_acquire);
+            if (i >= used_) continue;  // set_threads() left this worker out of the job
             const size_t lo = (size_t)i * chunk_;
             if (lo < n_) nt_copy(dst_ + lo, src_ + lo, (lo + chunk_ < n_ ? chunk_ : n_ - lo));
             pending_.fetch_sub(1, std::memory_order_release);
@@ -173,6 +186,8 @@ class CopyPool {
     const char* src_ = nullptr;
     size_t n_ = 0, chunk_ = 0;
     std::atomic<int> pending_{0};
+    std::atomic<int> active_{1 << 20};
+    int used_ = 0;
     std::atomic<bool> forked_{false};
 };
 
@@ -188,6 +203,9 @@ bool is_pinned(const void* p) {
 
 }  // namespace
 }  // namespace odx
+
+extern "C" int odx_host_threads_max(void) { return odx::CopyPool::get().max_threads(); }
+extern "C" int odx_set_host_threads(int n) { return odx::CopyPool::get().set_threads(n); }
 
 extern "C" int odx_solve_host(const odx_problem* P, const odx_stepper* S, const double* x0,
                               const double* X_guess, double* X_out, int64_t B, int64_t N,

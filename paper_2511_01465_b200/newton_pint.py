@@ -31,6 +31,8 @@ __all__ = [
     "Trajectory", "NewtonConfig", "SolveReport", "BatchSolveReport",
     "SingularDiagonalBlockError", "NonFiniteError", "n_steps_for", "initial_guess", "solve",
     "solve_batch", "solve_device", "GUESS_POLICIES", "initial_guess_device",
+    "residual_explicit", "residual_implicit", "newton_step_explicit", "newton_step_implicit",
+    "dense_jacobian_explicit", "dense_jacobian_implicit",
 ]
 
 GUESS_POLICIES = ("ones", "zeros", "replicate_x0", "coarse_euler")
@@ -203,6 +205,100 @@ def initial_guess_device(policy: str, problem: OdeProblem, n_steps: int, x0s=Non
     N.check(N.lib().odx_initial_guess(problem.native(), _GUESS_IDS[policy], N.ptr(x0t), N.ptr(X),
                                       B, n_steps, float(dt), N.stream_handle(dev)))
     return X
+
+
+# ---------------------------------------------------------------------------
+# List-based Newton steps and the dense Jacobian (newton_pint.py:210-312).
+# Host-side small-N forms of what the device solve does in one pass: the
+# reference keeps them as oracles (criterion 2: one Newton step == -H^-1 h),
+# and so do the tests here — tests/test_gpu_newton_step.py checks the device
+# solve's first update against them.
+# ---------------------------------------------------------------------------
+
+def _prev_row(traj: Trajectory, k: int) -> np.ndarray:
+    return traj.x0 if k == 0 else traj.states[k - 1]
+
+
+def _need_kind(stepper: StepperIncrement, kind: str) -> None:
+    if stepper.kind != kind:
+        raise ValueError(f"expected an {kind} stepper, got {stepper.kind!r}")
+
+
+def residual_explicit(traj: Trajectory, stepper: StepperIncrement) -> list:
+    """h_k = x_k - x_{k-1} - g(x_{k-1}) for every step (newton_pint.py:214-222)."""
+    _need_kind(stepper, "explicit")
+    return [traj.states[k] - _prev_row(traj, k) - stepper.eval(_prev_row(traj, k), traj.dt)
+            for k in range(traj.n_steps)]
+
+
+def residual_implicit(traj: Trajectory, stepper: StepperIncrement) -> list:
+    """h_k = x_k - x_{k-1} - g(x_{k-1}, x_k) for every step (newton_pint.py:225-234)."""
+    _need_kind(stepper, "implicit")
+    return [traj.states[k] - _prev_row(traj, k)
+            - stepper.eval(_prev_row(traj, k), traj.states[k], traj.dt)
+            for k in range(traj.n_steps)]
+
+
+def _scan_states(F_seq, c_seq, d: int) -> list:
+    from .affine_scan import extract_states, init_elements, scan_parallel
+    return extract_states(scan_parallel(init_elements(F_seq, c_seq, np.zeros(d))))
+
+
+def newton_step_explicit(traj: Trajectory, residual_blocks, stepper: StepperIncrement) -> list:
+    """Newton-step blocks u_1..u_N through the list scan, explicit step map
+    (newton_pint.py:237-250): element k is (I + dg/dx(x_{k-1}), -h_k), F_0 = 0."""
+    _need_kind(stepper, "explicit")
+    n, d = traj.n_steps, traj.dim
+    F_seq = [np.zeros((d, d))] + [np.eye(d) + stepper.jac_prev(traj.states[k - 1], traj.dt)
+                                  for k in range(1, n)]
+    c_seq = [-np.asarray(r, dtype=np.float64) for r in residual_blocks]
+    return _scan_states(F_seq, c_seq, d)
+
+
+def newton_step_implicit(traj: Trajectory, residual_blocks, stepper: StepperIncrement) -> list:
+    """Newton-step blocks with per-block diagonal solves (newton_pint.py:253-275):
+    element k is (A_k^-1 (I + dg/dx_prev), A_k^-1 (-h_k)), A_k = I - dg/dx_next.
+    A singular A_k raises SingularDiagonalBlockError(k)."""
+    from .linalg_small import SingularMatrixError, lu_solve
+    _need_kind(stepper, "implicit")
+    n, d = traj.n_steps, traj.dim
+    eye = np.eye(d)
+    F_seq, c_seq = [], []
+    for k in range(n):
+        prev, nxt = _prev_row(traj, k), traj.states[k]
+        A = eye - stepper.jac_next(prev, nxt, traj.dt)
+        try:
+            F_seq.append(np.zeros((d, d)) if k == 0 else
+                         lu_solve(A, eye + stepper.jac_prev(prev, nxt, traj.dt)))
+            c_seq.append(lu_solve(A, -np.asarray(residual_blocks[k], dtype=np.float64)))
+        except SingularMatrixError as exc:
+            raise SingularDiagonalBlockError(k) from exc
+    return _scan_states(F_seq, c_seq, d)
+
+
+def dense_jacobian_explicit(traj: Trajectory, stepper: StepperIncrement) -> np.ndarray:
+    """The assembled (N d x N d) Jacobian of the explicit rollout (newton_pint.py:278-295):
+    identity diagonal blocks, sub-diagonal blocks -I - dg/dx(x_{k-1})."""
+    n, d = traj.n_steps, traj.dim
+    H = np.kron(np.eye(n), np.eye(d))
+    for k in range(1, n):
+        H[k * d:(k + 1) * d, (k - 1) * d:k * d] = (
+            -np.eye(d) - stepper.jac_prev(traj.states[k - 1], traj.dt))
+    return H
+
+
+def dense_jacobian_implicit(traj: Trajectory, stepper: StepperIncrement) -> np.ndarray:
+    """The assembled Jacobian of the implicit rollout (newton_pint.py:298-312):
+    diagonal blocks I - dg/dx_next, sub-diagonal blocks -I - dg/dx_prev."""
+    n, d = traj.n_steps, traj.dim
+    eye = np.eye(d)
+    H = np.zeros((n * d, n * d))
+    for k in range(n):
+        prev, nxt = _prev_row(traj, k), traj.states[k]
+        H[k * d:(k + 1) * d, k * d:(k + 1) * d] = eye - stepper.jac_next(prev, nxt, traj.dt)
+        if k > 0:
+            H[k * d:(k + 1) * d, (k - 1) * d:k * d] = -eye - stepper.jac_prev(prev, nxt, traj.dt)
+    return H
 
 
 def _resolve_guess(guess, problem: OdeProblem, n: int, dt: float) -> Trajectory:
