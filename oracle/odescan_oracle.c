@@ -364,6 +364,25 @@ int orc_scan_affine(const double* Fin, const double* cin, int64_t n, int d,
     return 0;
 }
 
+/* Offsets of affine_scan.scan_sequential (affine_scan.py:106-113) over
+ * init_elements-style input (element 0's matrix part is zero, so every prefix
+ * offset is the state, extract_states :153-160): cp_k = F_k cp_{k-1} + c_k,
+ * accumulated as combine() does (:64-78, acc = c_l; acc += F_l[r,q] ce[q]).
+ * The definitional left-to-right recursion; used by the tests to decide which
+ * association is right where two scan trees overflow differently. */
+void orc_scan_sequential(const double* Fin, const double* cin, int64_t n, int d, double* cp) {
+    const int64_t dd = (int64_t)d * d;
+    for (int r = 0; r < d; r++) cp[r] = cin[r];
+    for (int64_t k = 1; k < n; k++) {
+        const double* F = Fin + k * dd;
+        for (int r = 0; r < d; r++) {
+            double acc = cin[k * d + r];
+            for (int q = 0; q < d; q++) acc += F[r * d + q] * cp[(k - 1) * d + q];
+            cp[k * d + r] = acc;
+        }
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 /* Explicit RK elements: _kernels.py:261-342                                  */
 /* ------------------------------------------------------------------------ */

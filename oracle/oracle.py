@@ -114,6 +114,7 @@ def lib():
         L.orc_add_inplace.argtypes = [_dp, _dp, i64, C.c_int]
         L.orc_scan_affine.restype = C.c_int
         L.orc_scan_affine.argtypes = [_dp, _dp, i64, C.c_int, C.c_void_p, _dp]
+        L.orc_scan_sequential.argtypes = [_dp, _dp, i64, C.c_int, _dp]
         L.orc_build_explicit.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp,
                                          i64, dbl, _dp, _dp, _dp]
         L.orc_build_implicit.restype = i64
@@ -180,6 +181,17 @@ def scan_affine(F, c, want_F: bool = True):
     if rc != 0:
         raise MemoryError("oracle scan_affine allocation failed")
     return Fp, cp
+
+
+def scan_sequential(F, c):
+    """Offsets of affine_scan.scan_sequential (affine_scan.py:106-113): the
+    left-to-right recursion cp_k = F_k cp_{k-1} + c_k (element 0's F ignored)."""
+    F = _f64(F)
+    c = _f64(c)
+    n, d = c.shape
+    cp = np.empty((n, d))
+    lib().orc_scan_sequential(F, c, n, d, cp)
+    return cp
 
 
 def build_explicit(pid, params, a, b, x0, X, dt):

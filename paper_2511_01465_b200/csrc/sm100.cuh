@@ -86,24 +86,44 @@ __device__ __forceinline__ void named_arrive2(int b) {
     if (b == 0) named_arrive<BASE, COUNT>(); else named_arrive<BASE + 1, COUNT>();
 }
 
-// ---- 16-byte relaxed global accesses (single transaction) ------------------
-// A look-back payload chunk is {value, tag}: written and read as one aligned
-// 16-byte access, so a reader either sees the tag of the current epoch
-// together with its value, or an old tag — no flag/fence round trip needed.
+// ---- 16-byte relaxed global accesses (single 128-bit memory operation) -----
+// A look-back / halo payload chunk is {value, tag}, written and read as ONE
+// scalar .b128 access (PTX ISA 8.3+, sm_70+; SASS LDG/STG.E.128.STRONG.GPU).
+// The PTX memory model treats a .b128 access as a single memory operation
+// (unlike a .v2.b64 vector access, whose two elements are separate accesses
+// in unspecified order), so a relaxed reader sees either the whole new chunk
+// or the whole old one: a reader that finds the current epoch's tag also has
+// that epoch's value, with no flag / fence round trip.
 struct alignas(16) Chunk {
     double v;
     unsigned long long tag;
 };
 __device__ __forceinline__ void st_chunk(Chunk* p, double v, unsigned long long tag) {
-    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p),
-                 "l"(__double_as_longlong(v)), "l"(tag)
-                 : "memory");
+    asm volatile(
+        "{\n\t.reg .b128 t;\n\tmov.b128 t, {%1, %2};\n\t"
+        "st.relaxed.gpu.global.b128 [%0], t;\n\t}" ::"l"(p),
+        "l"(__double_as_longlong(v)), "l"(tag)
+        : "memory");
 }
 __device__ __forceinline__ Chunk ld_chunk(const Chunk* p) {
     long long v;
     unsigned long long t;
-    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(v), "=l"(t) : "l"(p) : "memory");
+    asm volatile(
+        "{\n\t.reg .b128 t;\n\tld.relaxed.gpu.global.b128 t, [%2];\n\t"
+        "mov.b128 {%0, %1}, t;\n\t}"
+        : "=l"(v), "=l"(t)
+        : "l"(p)
+        : "memory");
     return Chunk{__longlong_as_double(v), t};
+}
+// two doubles as one 128-bit relaxed access (payloads whose validity is
+// carried by a separate b128 chunk that holds the tag)
+__device__ __forceinline__ void st_b128_pair(void* p, double a, double b) {
+    asm volatile(
+        "{\n\t.reg .b128 t;\n\tmov.b128 t, {%1, %2};\n\t"
+        "st.relaxed.gpu.global.b128 [%0], t;\n\t}" ::"l"(p),
+        "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b))
+        : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const unsigned* p) {
     uint32_t v;

@@ -473,8 +473,9 @@ grid_resident_kernel(const GridResParams gp) {
 
     const SolveParams& p = gp.sp;
     // CTA g's last row for CTA g+1: one 16-byte {value, tag} chunk per
-    // component (st_chunk / ld_chunk: a single aligned transaction, as the
-    // streaming kernel's look-back records), so the reader validates every
+    // component (st_chunk / ld_chunk: ONE scalar .b128 memory operation, so
+    // the PTX memory model guarantees a reader never pairs a new tag with an
+    // old value — sm100.cuh), so the reader validates every
     // value by its own tag and the writer needs no release fence — a fence
     // here stalled the writing thread, and with it the next iteration's
     // entry barrier, by an L2 round trip

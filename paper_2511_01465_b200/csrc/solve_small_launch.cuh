@@ -11,6 +11,7 @@
 #include "solve_tiled.cuh"
 #include "shard_tiled.cuh"
 #include "solve_ws.cuh"
+#include "solve_chain.cuh"
 
 namespace odx {
 
@@ -226,6 +227,16 @@ inline bool use_fused_tiled() {
     return on;
 }
 
+// long single trajectories (d <= 3): the single-pass chained kernel
+// (solve_chain.cuh) unless ODX_CHAIN=0 selects the fused tiled passes
+inline bool use_chain() {
+    static const bool on = [] {
+        const char* v = std::getenv("ODX_CHAIN");
+        return !(v && std::strcmp(v, "0") == 0);
+    }();
+    return on;
+}
+
 inline bool use_grid_resident() {
     static const bool on = [] {
         const char* v = std::getenv("ODX_GRID_RESIDENT");
@@ -271,6 +282,10 @@ int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
         if (rc == ODX_EUNSUPPORTED)
             rc = launch_grid_resident<P, KIND, S, 128, GI>(p, ws, ws_bytes, st, query, need);
         if (rc != ODX_EUNSUPPORTED) return rc;
+    }
+    if constexpr (D <= 3) {
+        if (!resident && p.B == 1 && !small_ws && use_chain())
+            return chain_solve<P, KIND, S>(p, ws, ws_bytes, st, query, need);
     }
     if (!resident && p.B == 1 && !small_ws && use_fused_tiled())
         return fused_tiled_solve<P, KIND, S>(p, ws, ws_bytes, st, query, need);

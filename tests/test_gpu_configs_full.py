@@ -45,28 +45,151 @@ def cfg5_trace(oracle):
                         cfg.dt, 10, abort_nonfinite=False, trace=True)
 
 
+@pytest.fixture(scope="module")
+def cfg5_seq_trace(oracle):
+    """The same 10 iterations with the reference's OTHER scan — the definitional
+    left-to-right recursion (affine_scan.scan_sequential, oracle.scan_sequential)
+    instead of the Blelloch tree of _kernels.scan_affine.  Where the iterates
+    diverge (|x| up to 1e308) the Newton map amplifies a rounding difference
+    between two association orders; the distance between these two REFERENCE
+    trajectories measures that amplification per iterate."""
+    from paper_2511_01465_b200.configs import CONFIGS
+    cfg = CONFIGS[5]
+    n = cfg.oracle_n_steps
+    x0 = cfg.x0s()[0]
+    st = oracle.stepper_by_name("rk4")
+    a = np.array([st.a[i] for i in range(16)]).reshape(4, 4)
+    b = np.array([st.b[i] for i in range(4)])
+    X = np.tile(x0, (n, 1))
+    out = [X.copy()]
+    for _ in range(10):
+        Fe, ce, _ = oracle.build_explicit(1, cfg.params, a, b, x0, X, cfg.dt)
+        X = X + oracle.scan_sequential(Fe, ce)
+        out.append(X.copy())
+    return out
+
+
+def _scaled_gap(A, B):
+    both = _rows_finite(A) & _rows_finite(B)
+    if not both.any():
+        return 0.0
+    scale = max(1.0, float(np.abs(B[both]).max()))
+    return float(np.abs(A[both] - B[both]).max()) / scale
+
+
 def _rows_finite(X):
     return np.isfinite(X).all(axis=1)
 
 
-def test_cfg5_2p22_every_iterate(pkg, cfg5_trace):
+DBL_MAX = np.finfo(np.float64).max
+
+
+def _overflow_boundary_ok(X, R, Xprev, cfg, oracle, what):
+    """Rows where the GPU iterate and the reference differ in finiteness must be
+    overflow-boundary rows: the finite side is within one binade of DBL_MAX, and
+    the DEFINITIONAL recursion — affine_scan.scan_sequential (affine_scan.py:
+    106-113, restated as oracle.scan_sequential) over the reference's own
+    elements built at the previous iterate — agrees with the GPU there.  The
+    reference's Blelloch tree (_kernels.py:116-233) forms F products over spans
+    of up to N/2 steps; on a trajectory growing like 1.00045^k those products
+    overflow (inf * finite c = inf) at rows whose true value is still finite,
+    so the tree's first inf can precede the recursion's by a few rows.
+    Returns the number of such rows; every other row's mask must match."""
+    fr, fx = _rows_finite(R), _rows_finite(X)
+    bad = np.nonzero(fr != fx)[0]
+    if bad.size == 0:
+        return 0
+    assert bad.size <= 64, f"{what}: {bad.size} rows differ in finiteness"
+    x0 = cfg.x0s()[0]
+    st = oracle.stepper_by_name("rk4")
+    a = np.array([st.a[i] for i in range(16)]).reshape(4, 4)
+    b = np.array([st.b[i] for i in range(4)])
+    Fe, ce, _ = oracle.build_explicit(1, cfg.params, a, b, x0, Xprev, cfg.dt)
+    Xseq = Xprev + oracle.scan_sequential(Fe, ce)
+    fs = _rows_finite(Xseq)
+    for r in bad:
+        fin = X[r] if fx[r] else R[r]
+        assert np.isfinite(fin).all() and np.abs(fin).max() > DBL_MAX / 2, (
+            f"{what}: row {r} differs in finiteness away from the overflow boundary "
+            f"(gpu {X[r]}, ref {R[r]})")
+        # the recursion decides: GPU agrees with it in finiteness and value —
+        # up to a value within rounding of DBL_MAX itself (finite in one
+        # association, inf in the other)
+        if fs[r] != fx[r]:
+            fin2 = X[r] if fx[r] else Xseq[r]
+            assert np.abs(fin2).max() > DBL_MAX * (1.0 - 1e-3), (
+                f"{what}: row {r}: gpu {X[r]}, recursion {Xseq[r]}")
+        elif fs[r]:
+            scale = np.abs(Xseq[r]).max()
+            assert np.abs(X[r] - Xseq[r]).max() <= 1e-9 * scale, (what, r, X[r], Xseq[r])
+    return int(bad.size)
+
+
+def _cfg5_setup(pkg):
     from paper_2511_01465_b200.configs import CONFIGS
     cfg = CONFIGS[5]
     n = cfg.oracle_n_steps
+    prob = pkg.van_der_pol(mu=cfg.params[0], x0=cfg.x0s()[0], tf=n * cfg.dt)
+    return cfg, n, prob, pkg.get_stepper("rk4", prob)
+
+
+def test_cfg5_2p22_every_iterate(pkg, oracle, cfg5_trace, cfg5_seq_trace):
+    """The production run (constant-x0 guess, k = 1..10 iterations) against the
+    oracle's trace: masks (overflow-boundary rule at iterate 2), residual
+    histories, SURVEY's 10,509-row finite prefix, and the scaled error —
+    1e-9, or 10x the distance between the reference's two scans' trajectories
+    (tree vs sequential recursion, cfg5_seq_trace) where the diverging
+    iterates amplify association differences beyond that.  Every single
+    Newton step is held to 1e-9 by test_cfg5_2p22_each_step_from_reference."""
+    cfg, n, _, _ = _cfg5_setup(pkg)
     ref = cfg5_trace
     assert int(_rows_finite(ref["X"]).sum()) == 10_509  # SURVEY Appendix A (reference kernels)
     assert int(_rows_finite(ref["X"]).argmin()) == 10_509  # a finite PREFIX, then NaN
     assert np.isnan(ref["X"][10_509:]).all()
+    boundary = {}
     for k in range(1, 11):
         r = _gpu_cfg_solve(pkg, cfg, n=n, max_iters=k)
         assert int(r.status[0]) == 0 and int(r.iterations_run[0]) == k
-        scaled_close(r.states[0], ref["trace"][k], TOL, f"cfg5 2^22 iterate {k}")
+        X, R = r.states[0], ref["trace"][k]
+        nb = _overflow_boundary_ok(X, R, ref["trace"][k - 1], cfg, oracle, f"iterate {k}")
+        boundary[k] = nb
+        both = _rows_finite(X) & _rows_finite(R)
+        gap = _scaled_gap(cfg5_seq_trace[k], R)
+        tol = max(TOL, 10.0 * gap)
+        print(f"iterate {k}: gpu scaled err {_scaled_gap(X, R):.3e}, tree-vs-sequential "
+              f"{gap:.3e}, bound {tol:.1e}")
+        scaled_close(X[both], R[both], tol, f"cfg5 2^22 iterate {k}")
+        if nb == 0:
+            scaled_close(X, R, tol, f"cfg5 2^22 iterate {k}")
         h = r.residual_history[0]
         # the plain history: NaN-ignoring max|h| (inf from iterate 2 on)
         assert np.array_equal(np.isinf(h), np.isinf(ref["hist"][:k + 1]))
         fin = np.isfinite(ref["hist"][:k + 1])
         np.testing.assert_allclose(h[fin], ref["hist"][:k + 1][fin], rtol=1e-7)
+    # only iterate 2 (the first overflow) may have boundary rows; from iterate 3
+    # on the masks are identical, and the final finite prefix is SURVEY's 10,509
+    assert all(v == 0 for k, v in boundary.items() if k != 2), boundary
     assert int(_rows_finite(r.states[0]).sum()) == 10_509
+
+
+def test_cfg5_2p22_each_step_from_reference(pkg, oracle, cfg5_trace):
+    """Each Newton step of cfg5 in isolation, on the production route at the
+    oracle size: one GPU iteration from the reference's iterate k-1 against
+    the reference's iterate k (k = 1..10) at 1e-9 scaled, masks by the
+    overflow-boundary rule.  (A single step of the definitional sequential
+    recursion differs from the reference's tree by <= 1.3e-11 here.)"""
+    from paper_2511_01465_b200.newton_pint import solve_batch
+    cfg, n, prob, st = _cfg5_setup(pkg)
+    conf = pkg.NewtonConfig(max_iters=1, abort_on_nonfinite=False)
+    for k in range(1, 11):
+        G = np.ascontiguousarray(cfg5_trace["trace"][k - 1])
+        r = solve_batch(prob, st, cfg.dt, cfg.x0s(), G[None], conf)
+        X, R = r.states[0], cfg5_trace["trace"][k]
+        nb = _overflow_boundary_ok(X, R, G, cfg, oracle, f"step {k}")
+        both = _rows_finite(X) & _rows_finite(R)
+        scaled_close(X[both], R[both], TOL, f"cfg5 2^22 step {k}")
+        if nb == 0:
+            scaled_close(X, R, TOL, f"cfg5 2^22 step {k}")
 
 
 def test_cfg5_2p22_time_sharded_8_ranks(pkg, cfg5_trace):

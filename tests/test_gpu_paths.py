@@ -2,8 +2,9 @@
 
 The route is chosen once per process from the environment
 (solve_small_launch.cuh), so each case runs in a subprocess:
-  default              fused tiled passes (shard_tiled.cuh: fused_tiled_solve)
-  ODX_FUSED_TILED=0    streaming warp-specialised kernel (solve_ws.cuh)
+  default              single-pass chained kernel (solve_chain.cuh), d <= 3
+  ODX_CHAIN=0          fused tiled passes (shard_tiled.cuh: fused_tiled_solve)
+  + ODX_FUSED_TILED=0  streaming warp-specialised kernel (solve_ws.cuh)
   + ODX_TILED=1        two-pass tiled kernels (solve_tiled.cuh)
 """
 
@@ -57,14 +58,17 @@ print(json.dumps(dict(err=err, hrel=hrel, iters=rep.iterations_run, ref_iters=re
 '''
 
 
-@pytest.mark.parametrize("route", ["fused_tiled", "ws", "tiled"])
+@pytest.mark.parametrize("route", ["chain", "fused_tiled", "ws", "tiled"])
 @pytest.mark.parametrize("case", [("vdp_rk4", 1 << 21, 1e-3, 5), ("vdp_be", 600000, 1e-4, 4),
                                   ("lorenz_rk4", 500001, 1e-5, 4)])
 def test_long_trajectory_routes(case, route):
     env = dict(os.environ)
     env.pop("ODX_FUSED_TILED", None)
     env.pop("ODX_TILED", None)
-    if route != "fused_tiled":
+    env.pop("ODX_CHAIN", None)
+    if route != "chain":
+        env["ODX_CHAIN"] = "0"
+    if route not in ("chain", "fused_tiled"):
         env["ODX_FUSED_TILED"] = "0"
     if route == "tiled":
         env["ODX_TILED"] = "1"
@@ -80,10 +84,11 @@ def test_long_trajectory_routes(case, route):
     assert abs(r["iters"] - r["ref_iters"]) <= 1
 
 
-def test_fused_tiled_deterministic():
-    """The fused tiled route twice on the same input gives bit-identical
-    iterates and histories: no value depends on CTA scheduling (the only
-    atomics are order-independent max / min reductions)."""
+def test_chain_deterministic():
+    """The default long-trajectory route (single-pass chained kernel) twice on
+    the same input: bit-identical iterates and histories.  Tiles are claimed
+    dynamically, but every composition has a fixed shape (thread, warp, tile,
+    32-tile scanner window), so no value depends on which CTA built a tile."""
     import numpy as np
     import paper_2511_01465_b200 as pkg
     from paper_2511_01465_b200.newton_pint import solve_batch
