@@ -1,27 +1,36 @@
 #!/usr/bin/env python
 """Benchmark of the B200 parallel-in-time Newton solver (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5]
                     [--impl ours|reference]
 
 Metric: Newton time-steps/s = (trajectories x N steps x Newton iterations) / s.
 
-Workload (config.workload): BASELINE.json configs[1] = cfg2, van der Pol
-mu=10, backward Euler, N=65536, d=2, fp64.  One bench step = one solve of that
-trajectory running a FIXED 10 Newton iterations in the non-aborting timing
-mode (under BASELINE's own stop rule cfg2 ends NONFINITE after 2
-updates, so the stable steps/s figure is taken at a fixed iteration count; the
-stop-rule solve is timed too and reported under "stop_rule").  Inputs are
-resident in HBM when the timed region starts; L2 (126 MB) is flushed between
-steps because the 1 MB state would otherwise stay cached across solves.  Each
-step is timed with its own CUDA-event pair on the launching stream.
+Headline workload (config.workload): BASELINE.json configs[4] = cfg5, van der
+Pol mu=1, explicit RK4 h=1e-3, N = 2^26 steps, d=2, fp64, constant-x0 initial
+guess, timed over a FIXED 10 Newton iterations (BASELINE's own definition of
+cfg5) — the largest single-GPU configuration.  One bench step =
+one such solve.  Inputs are resident in HBM when the timed region starts (the
+1 GiB state is larger than the 126 MB L2, which is also flushed between steps);
+each step is timed with its own CUDA-event pair on the launching stream.
 
-Every other BASELINE config is measured the same way and reported under
-"configs" (cfg5 at N=2^26 is the HBM-scale case).
+`e2e` = the same solve through the public API a user calls —
+`solve(problem, stepper, dt, guess="replicate_x0", config)` (newton_pint.py
+mirror of the reference's solve()): the constant guess is built on the device
+from x0 (the only host->device input), and the 1 GiB trajectory comes back to a
+host numpy array inside the timed region.
+
+At N > 1 GPUs (torchrun) the headline is the same trajectory split along time
+over the ranks (sharded.py: one NCCL all-gather of per-rank records per
+Newton iteration): strong scaling; e2e there copies each rank's chunk of the
+guess host->device and its chunk of the result back.
+
+Every other BASELINE config is measured at N = 1 under "configs".
 
 --impl reference times the reference's CPU implementation of the path — the
 C restatement in oracle/ (bit-identical to the numba reference, see
-tests/test_oracle_golden.py) on all host cores — on the same workload.
+tests/test_oracle_golden.py) on all host cores — on the same workload at the
+size BASELINE allows for the CPU (cfg5: N = 2^22, reported per step).
 """
 
 from __future__ import annotations
@@ -60,7 +69,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--iters", type=int, default=10, help="fixed Newton iterations per step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -139,7 +148,8 @@ def peaks():
     if FP64_PEAK.exists():
         try:
             fp64 = float(json.loads(FP64_PEAK.read_text())["dfma_gflops"])
-            fsrc = "measured (profiles/fp64_peak.json, DFMA)"
+            fsrc = ("builder-measured: profiles/fp64_peak.json (tools/fp64_peak.cu DFMA loop "
+                    "on this pool's B200; MEASURED_PEAKS.json has no fp64 entry)")
         except (KeyError, ValueError):
             pass
     return hbm, src, fp64, fsrc
@@ -271,12 +281,24 @@ class TimeShardedWorkload:
         return (np.array([r.iterations_run]), np.array([r.status]), np.array([r.status_index]))
 
 
-# the device path each BASELINE config runs (kernel table)
-ROUTE = {1: "resident_solve_kernel (one CTA, 256 threads x 4 steps)",
-         2: "grid_resident_kernel (128 co-resident CTAs x 512 steps)",
-         3: "resident_solve_kernel (one CTA per trajectory, 256 x 8)",
-         4: "dense_band/lu_build + dense_agg (DMMA) + dense_fold + dense_fixup",
-         5: "tiled_build + per iteration shard_step_carry / shard_fused / shard_scan_record"}
+def route_of(w) -> str:
+    """The device path the library reports for the last solve (odx_last_route)."""
+    if isinstance(w, TimeShardedWorkload):
+        return ("time-sharded: per rank shard_fused_kernel + one NCCL all-gather of the "
+                "rank records per Newton iteration (sharded.py, protocol 'device')")
+    r = w.N.lib().odx_last_route()
+    return r.decode() if r else "unknown"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def flush_l2(buf):
@@ -309,28 +331,73 @@ def time_steps(w: Workload, steps: int, warmup: int, flush):
 
 
 def e2e_steps(w: Workload, steps: int, warmup: int):
-    """Same metric through the public API with HOST buffers: solve_batch(numpy)."""
+    """Same metric through the public API with HOST buffers.
+
+    cfg5 (one trajectory, constant-x0 guess): solve(problem, stepper, dt,
+    guess="replicate_x0") — the guess is built on the device from x0 and the
+    trajectory is returned as a host numpy array.  Batched / other configs:
+    solve_batch(numpy x0s, numpy guess) -> numpy states."""
     torch = w.torch
     import paper_2511_01465_b200 as pkg
     from paper_2511_01465_b200.newton_pint import solve_batch
     conf = pkg.NewtonConfig(max_iters=w.iters, abort_on_nonfinite=False)
     x0_host = w.x0.cpu().numpy()
-    guess_host = np.ascontiguousarray(np.broadcast_to(w.host_guess, (w.B, w.n, w.d)))
+    if w.B == 1 and w.cid == 5:
+        def call():
+            return pkg.solve(w.prob, w.stepper, w.cfg.dt, guess="replicate_x0", config=conf)
+        h2d = x0_host.nbytes
+        guess_note = "replicate_x0 policy built on the device (odx_initial_guess) from x0"
+    else:
+        guess_host = np.ascontiguousarray(np.broadcast_to(w.host_guess, (w.B, w.n, w.d)))
+
+        def call():
+            return solve_batch(w.prob, w.stepper, w.cfg.dt, x0_host, guess_host, conf)
+        h2d = guess_host.nbytes + x0_host.nbytes
+        guess_note = "host numpy guess (B, N, d) copied in"
     for _ in range(warmup):
-        solve_batch(w.prob, w.stepper, w.cfg.dt, x0_host, guess_host, conf)
+        call()
     torch.cuda.synchronize()
     durs = []
+    rep = None
     for _ in range(steps):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        rep = solve_batch(w.prob, w.stepper, w.cfg.dt, x0_host, guess_host, conf)
+        rep = call()
         e1.record()
         torch.cuda.synchronize()
         durs.append(e0.elapsed_time(e1))
-    h2d = guess_host.nbytes + x0_host.nbytes
-    d2h = rep.states.nbytes + rep.residual_history.nbytes * 2 + w.B * (4 + 4 + 8)
-    return durs, h2d, d2h
+        del rep
+    H = w.iters + 1
+    d2h = w.B * w.n * w.d * 8 + w.B * (2 * H * 8 + 4 + 4 + 8)
+    return durs, h2d, d2h, guess_note
+
+
+def sharded_e2e(tw, steps: int, warmup: int, world: int):
+    """Time-sharded e2e: each rank copies its chunk of the host guess in, runs
+    its part of the solve and copies its chunk of the trajectory out; max over
+    ranks of the event-timed step."""
+    torch = tw.torch
+    from paper_2511_01465_b200.sharded import solve_time_sharded
+    host_guess = tw.guess.cpu().numpy()
+    durs = []
+    for k in range(warmup + steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        tw.X.copy_(torch.from_numpy(host_guess), non_blocking=False)
+        solve_time_sharded(tw.prob, tw.stepper, tw.cfg.dt, tw.X, tw.off, tw.conf)
+        out = tw.X.cpu()
+        e1.record()
+        torch.cuda.synchronize()
+        if k >= warmup:
+            durs.append(e0.elapsed_time(e1))
+        del out
+    tot = reduce_max(sum(durs), world)
+    nb = host_guess.nbytes
+    return tot / len(durs), nb, nb
 
 
 def reduce_max(v: float, world: int) -> float:
@@ -355,12 +422,15 @@ def roofline_for(cid, n, B, iters, avg_ms, hbm, hbm_src, fp64, fp64_src):
     tf = flops / t / 1e9  # GFLOP/s
     ai = alg["flops"] / alg["bytes"]
     ridge = fp64 / hbm
+    note = ("achieved = algorithmic work per solve (SURVEY 8(d)/Appendix B: 16*d bytes and the "
+            "reference-equivalent flops per step per iteration; the last, build-only pass reads x "
+            "once) / device time of the solve (all its launches, back to back on one stream)")
     if ai > ridge:
-        return {"bound": "fp64", "achieved": round(tf, 1), "peak": fp64, "unit": "GFLOP/s",
+        return {"bound": "fp64", "note": note, "achieved": round(tf, 1), "peak": fp64, "unit": "GFLOP/s",
                 "frac": round(tf / fp64, 4), "peak_source": fp64_src,
                 "hbm_achieved_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4),
                 "alg_bytes_per_launch": bytes_, "alg_flops_per_launch": flops, "traffic": None}
-    return {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+    return {"bound": "hbm", "note": note, "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(gbs / hbm, 4), "peak_source": hbm_src,
             "fp64_achieved_gflops": round(tf, 1), "fp64_frac": round(tf / fp64, 4),
             "alg_bytes_per_launch": bytes_, "alg_flops_per_launch": flops, "traffic": None}
@@ -391,10 +461,11 @@ def cpu_baseline(cid: int, iters: int, seconds: float, n_override=None):
         if el >= seconds:
             break
     val = runs * n * iters / el
-    sample = (f"{cfg.name}: {runs} oracle solve(s) of 1 trajectory x N={n} x {iters} fixed "
-              f"Newton iterations in {el:.1f} s")
+    sample = (f"{cfg.name}: {runs} solve(s) of 1 trajectory x N={n} x {iters} fixed Newton "
+              f"iterations in {el:.1f} s by the C port of the reference (oracle/odescan_oracle.c, "
+              f"bit-identical to its numba kernels), OpenMP on {cores} threads")
     return {"value": val, "unit": "Newton time-steps/s", "cores": cores, "kind": "port",
-            "sample": sample}
+            "cpu_model": cpu_model(), "sample": sample}
 
 
 def run_reference(args, world, rank):
@@ -427,18 +498,25 @@ def run_reference(args, world, rank):
         durs.append(time.perf_counter() - t0)
     tot = sum(durs)
     val = args.steps * n * args.iters / tot
-    sample = (f"{cfg.name}: per step one oracle solve of 1 trajectory x N={n} x {args.iters} "
-              f"fixed Newton iterations (C port of the reference, OpenMP {cores} threads)")
+    note = ("BASELINE configs[4]: the reference CPU is timed at N=2^22 and reported per step"
+            if cid == 5 else "cfg4's reference CPU cost is ~17 s per iteration at the full N; "
+            "timed at N=1024 and reported per step" if cid == 4 else "full configuration")
+    sample = (f"{cfg.name}: per step one solve of 1 trajectory x N={n} x {args.iters} fixed "
+              f"Newton iterations by the C port of the reference (oracle/odescan_oracle.c, "
+              f"bit-identical to the reference's numba kernels per tests/test_oracle_golden.py), "
+              f"OpenMP {cores} threads on {cpu_model()}; {note}")
     line = {
         "metric": "Newton time-steps/s (Jacobian+scan)", "value": val,
         "unit": "Newton time-steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if (cid == 5 and world > 1) else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (BASELINE.json configs, seeded default_rng(0))",
         "impl": "reference",
-        "config": {"workload": cfg.name, "n_steps": n, "batch": 1, "newton_iters": args.iters,
+        "config": {"workload": cfg.name, "n_steps": n, "n_steps_config": cfg.n_steps,
+                   "batch": 1, "newton_iters": args.iters,
                    "mode": "fixed iterations, non-aborting", "parallelism": "cpu"},
         "cpu_baseline": {"value": val, "unit": "Newton time-steps/s", "cores": cores,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": val, "unit": "Newton time-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -482,22 +560,33 @@ def main():
     it, st, ix = w.outcome()
 
     names = {0: "MAXITER", 1: "CONVERGED", 2: "NONFINITE", 3: "SINGULAR"}
+    path = route_of(w)
+    stop_rule = None
     if sharded_time:
-        e2e_ms, e2e_val, h2d, d2h = avg_ms, value, 0, 0
-        stop_rule = None
+        # e2e: each rank's guess chunk host->device, the sharded solve, its
+        # result chunk device->host (max over ranks)
+        e2e_ms, h2d, d2h = sharded_e2e(w, max(3, args.steps // 2), 1, world)
+        e2e_val = units_per_step / (e2e_ms * 1e-3)
+        guess_note = "host numpy guess chunk per rank copied in; result chunk copied out"
     else:
         # e2e through the public API with host buffers
-        e2e_durs, h2d, d2h = e2e_steps(w, max(5, args.steps), max(3, args.warmup))
+        e2e_durs, h2d, d2h, guess_note = e2e_steps(w, max(5, args.steps // 2),
+                                                   max(3, args.warmup))
         e2e_ms = reduce_max(sum(e2e_durs), world) / len(e2e_durs)
         e2e_val = units_per_step / (e2e_ms * 1e-3)
-        # BASELINE stop-rule solve of the same config
-        w.set_mode(fixed=False)
-        sr_durs, _ = time_steps(w, 5, 2, flush)
-        sit, sst, six = w.outcome()
-        sr_ms = statistics.median(sr_durs)
-        stop_rule = {"status": names.get(int(sst[0]), str(int(sst[0]))),
-                     "status_index": int(six[0]), "iterations": int(sit[0]), "solve_ms": sr_ms,
-                     "newton_steps_per_s": w.n * w.B * max(int(sit[0]), 1) / (sr_ms * 1e-3)}
+        if cid == 5:
+            stop_rule = {"note": "cfg5 is defined as a fixed 10-iteration solve (BASELINE "
+                                 "configs[4]); its rule is the timed solve itself"}
+        else:
+            # BASELINE stop-rule solve of the same config
+            w.set_mode(fixed=False)
+            sr_durs, _ = time_steps(w, 5, 2, flush)
+            sit, sst, six = w.outcome()
+            sr_ms = statistics.median(sr_durs)
+            stop_rule = {"status": names.get(int(sst[0]), str(int(sst[0]))),
+                         "status_index": int(six[0]), "iterations": int(sit[0]),
+                         "solve_ms": sr_ms,
+                         "newton_steps_per_s": w.n * w.B * max(int(sit[0]), 1) / (sr_ms * 1e-3)}
 
     roof = roofline_for(cid, w.n, w.B, args.iters, avg_ms, hbm, hbm_src, fp64, fp64_src)
     prof_traffic = REPO / "profiles" / "traffic.json"
@@ -511,10 +600,11 @@ def main():
 
     extra = {}
     if not args.no_extra and world == 1:
-        for ocid in (1, 3, 5, 4):
+        for ocid in (o for o in (1, 2, 3, 4, 5) if o != cid):
             try:
                 ow = Workload(ocid, args.iters)
                 od, _ = time_steps(ow, 5, 2, flush)
+                opath = route_of(ow)
                 oms = statistics.median(od)
                 ov = ow.B * ow.n * args.iters / (oms * 1e-3)
                 ow.set_mode(fixed=False)
@@ -522,7 +612,7 @@ def main():
                 oi, os_, ox = ow.outcome()
                 extra[ow.cfg.name] = {
                     "fixed_iters": args.iters, "ms": round(oms, 4), "newton_steps_per_s": ov,
-                    "path": ROUTE.get(ocid),
+                    "path": opath,
                     "roofline": roofline_for(ocid, ow.n, ow.B, args.iters, oms, hbm, hbm_src,
                                              fp64, fp64_src),
                     "stop_rule": {"ms": round(statistics.median(sd), 4),
@@ -580,8 +670,9 @@ def main():
                        "batch": w.B if cid == 3 else w.B * world,
                        "newton_iters": args.iters,
                        "mode": "fixed iterations, non-aborting (SURVEY 8d)",
-                       "l2": "flushed between steps (256 MB write)",
-                       "path": ROUTE.get(cid),
+                       "l2": ("inputs larger than L2 and L2 flushed between steps (256 MB write)"
+                              if w.n * w.d * 8 > 126e6 else "flushed between steps (256 MB write)"),
+                       "path": path,
                        "parallelism": ("single GPU" if world == 1 else
                                        f"time-sharded x{world}" if sharded_time else
                                        f"batch-sharded x{world}" if cid == 3 else
@@ -589,7 +680,10 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "Newton time-steps/s", "ms": e2e_ms,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "guess": guess_note,
+                    "api": ("sharded.solve_time_sharded per rank" if sharded_time else
+                            "solve(problem, stepper, dt, guess='replicate_x0', config) -> numpy"
+                            if cid == 5 else "solve_batch(numpy x0s, numpy guess) -> numpy")},
             "gpu_launches": launches,
             "clocks": clock_info,
             "final_status": {"iters": int(it[0]), "status": int(st[0])},

@@ -115,6 +115,9 @@ int         odx_supported(const odx_problem* P, const odx_stepper* S);
 /* Number of CUDA kernels this library has launched in this process (a
  * monotone counter, used to report `gpu_launches` in bench.py).            */
 int64_t     odx_launch_count(void);
+/* Name of the device path (kernel family) the last odx_solve / odx_solve_host
+ * on this host thread launched ("" before any): diagnostics and bench labels. */
+const char* odx_last_route(void);
 
 /* ---- the solver ------------------------------------------------------------
  * Replaces odescan.solve()  newton_pint.py:326-406 (batched over B

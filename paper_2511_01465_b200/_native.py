@@ -27,7 +27,8 @@ PROB_LINEAR = 10
 
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "odx_abi_version", "odx_last_error", "odx_supported", "odx_launch_count", "odx_solve_workspace_bytes",
+    "odx_abi_version", "odx_last_error", "odx_supported", "odx_launch_count", "odx_last_route",
+    "odx_solve_workspace_bytes",
     "odx_solve", "odx_solve_host", "odx_host_threads_max", "odx_set_host_threads",
     "odx_initial_guess", "odx_seq_march", "odx_parareal_coarse", "odx_build_explicit", "odx_build_implicit",
     "odx_scan_affine_workspace_bytes", "odx_scan_affine", "odx_max_abs", "odx_add_inplace",
@@ -77,6 +78,8 @@ def lib():
     L.odx_abi_version.restype = C.c_int
     L.odx_last_error.restype = C.c_char_p
     L.odx_launch_count.restype = C.c_int64
+    L.odx_last_route.restype = C.c_char_p
+    L.odx_last_route.argtypes = []
     L.odx_supported.restype = C.c_int
     L.odx_host_threads_max.restype = C.c_int
     L.odx_host_threads_max.argtypes = []

@@ -16,6 +16,7 @@ namespace odx {
 
 extern thread_local std::string g_err;
 extern std::atomic<long long> g_launches;
+extern thread_local const char* g_route;
 
 template <class P, int KIND, int S>
 int solve_small(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
@@ -195,6 +196,8 @@ const char* odx_last_error(void) { return g_err.c_str(); }
 
 int64_t odx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+const char* odx_last_route(void) { return g_route; }
+
 int odx_supported(const odx_problem* P, const odx_stepper* S) {
     if (check_problem(P, S) != ODX_OK) return 0;
     StepCoefs sc;
@@ -313,6 +316,7 @@ int odx_solve(const odx_problem* P, const odx_stepper* S, const double* x0, doub
               int32_t* iters, int32_t* status, int64_t* status_index, void* workspace,
               size_t workspace_bytes, void* stream) {
     g_err.clear();
+    g_route = "";
     SolveParams p;
     int rc = make_solve_params(P, S, x0, X, B, N, dt, C, hist, scaled_hist, iters, status,
                                status_index, p);

@@ -31,6 +31,8 @@ inline int fail(int code, const char* msg) {
 
 int num_sms();
 void count_launch(int n = 1);
+// names the device path the last solve on this host thread took (odx_last_route)
+void set_route(const char* route);
 
 // Sets the kernel's dynamic shared-memory limit and returns its resident CTAs
 // per SM, once per (kernel, block size, smem, device): both CUDA queries cost

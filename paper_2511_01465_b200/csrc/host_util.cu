@@ -22,6 +22,9 @@ void set_error(const char* fmt, ...) {
     g_err = buf;
 }
 
+thread_local const char* g_route = "";
+void set_route(const char* route) { g_route = route; }
+
 std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 

@@ -738,6 +738,7 @@ int fused_tiled_solve(const SolveParams& p, void* ws, size_t ws_bytes, cudaStrea
     fused_solve_finish_kernel<<<1, 1, 0, st>>>(state, p.iters, p.status, p.sidx);
     ODX_CUDA(cudaGetLastError());
     count_launch(1);
+    set_route("shard_fused_kernel (fused tiled passes, elements stored between passes)");
     return ODX_OK;
 }
 

@@ -797,6 +797,7 @@ int chain_solve(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
         free(h);
     }
     count_launch(p.max_iters + 3);  // init_ws + passes + finish
+    set_route("chain_pass_kernel (single pass per iteration: x read, x_new written; scanner CTA)");
     return ODX_OK;
 }
 

@@ -716,6 +716,7 @@ int dense_solve(const odx_problem* P, const odx_stepper* S, SolveParams& sp, voi
     dense_final_copy_kernel<<<(unsigned)(2 * num_sms()), 256, 0, st>>>(p);
     ODX_CUDA(cudaGetLastError());
     count_launch(launches + 1);
+    set_route("dense d=64: dense_band/lu_build + dense_agg (DMMA) + dense_fold + dense_fixup");
     return ODX_OK;
 }
 

@@ -27,6 +27,7 @@ int launch_resident(SolveParams& p, cudaStream_t st) {
     kern<<<(unsigned)p.B, THREADS, smem, st>>>(p);
     ODX_CUDA(cudaGetLastError());
     count_launch(1);
+    set_route("resident_solve_kernel (one CTA per trajectory, whole solve in one launch)");
     return ODX_OK;
 }
 
@@ -82,6 +83,7 @@ int launch_ws(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
                                          smem, st));
     ODX_CUDA(cudaGetLastError());
     count_launch(2);  // init_bad_slots + the persistent solve
+    set_route("persistent_ws_kernel (warp-specialised streaming look-back)");
     return ODX_OK;
 }
 
@@ -128,6 +130,7 @@ int launch_grid_resident(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t
                                          smem, st));
     ODX_CUDA(cudaGetLastError());
     count_launch(2);
+    set_route("grid_resident_kernel (one co-resident wave of CTAs, whole solve in one launch)");
     return ODX_OK;
 }
 
@@ -206,6 +209,7 @@ int launch_tiled(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, boo
     }
     ODX_CUDA(cudaGetLastError());
     count_launch(launches);
+    set_route("tiled_build/scan/apply_kernel (two-pass tiled)");
     return ODX_OK;
 }
 
