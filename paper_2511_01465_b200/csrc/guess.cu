@@ -103,6 +103,12 @@ inline dim3 guess_grid(long long B, long long N, int d) {
     return dim3((unsigned)per, (unsigned)B);
 }
 
+// validation only: with_small_problem's id / dim checks
+struct KnownProblem {
+    template <class Q>
+    int operator()() { return ODX_OK; }
+};
+
 struct GuessFn {
     ProbParams pp;
     int policy;
@@ -139,11 +145,7 @@ extern "C" int odx_initial_guess(const odx_problem* P, int32_t policy, const dou
     if (B > 65535) return fail(ODX_EINVAL, "B must be <= 65535");
     const bool dense = P->problem_id == ODX_PROB_ALLEN_CAHN && P->dim == 64;
     if (!dense) {  // the same problem / dim validation as the solve
-        struct Known {
-            template <class Q>
-            int operator()() { return ODX_OK; }
-        };
-        if (int rc = with_small_problem(P->problem_id, P->dim, Known{}))
+        if (int rc = with_small_problem(P->problem_id, P->dim, KnownProblem{}))
             return fail(rc, rc == ODX_EINVAL ? "problem does not have this dim"
                                              : "unknown problem id (no device functor)");
     }
