@@ -10,6 +10,7 @@
 //                        status -1, -(k+2) singular at k, or k (no convergence)
 #pragma once
 
+#include "common.cuh"
 #include "elements.cuh"
 
 namespace odx {
