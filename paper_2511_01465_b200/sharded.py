@@ -366,29 +366,36 @@ def solve_time_sharded(problem, stepper, dt: float, X_local, offset: int, config
                              status=out["status"], status_index=out["status_index"])
 
 
-def solve_batch_sharded(problem, stepper, dt: float, x0s, config, group=None):
+def solve_batch_sharded(problem, stepper, dt: float, x0s, config, group=None, solve_fn=None):
     """Batch sharding: contiguous slices of the B trajectories per rank.
 
     Runs solve_batch on this rank's slice (no collective on the data path) and
     all-gathers the per-trajectory statuses / iteration counts.  Returns
-    (local BatchSolveReport, offset, gathered dict).
+    (local BatchSolveReport, offset, gathered dict).  solve_fn(x0_slice) may
+    replace the device solve (the gloo tests run the CPU oracle there); the
+    status exchange then uses host tensors when the group is not NCCL.
     """
     import torch
     import torch.distributed as dist
     from .newton_pint import solve_batch
     R = dist.get_world_size(group)
     r = dist.get_rank(group)
-    B = int(np.asarray(x0s).shape[0])
+    x0s = np.asarray(x0s)
+    B = int(x0s.shape[0])
     off, nb = chunk_bounds(B, R, r)
-    rep = solve_batch(problem, stepper, dt, np.asarray(x0s)[off:off + nb], None, config)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    if solve_fn is None:
+        def solve_fn(xs):
+            return solve_batch(problem, stepper, dt, xs, None, config)
+    rep = solve_fn(x0s[off:off + nb])
+    dev = (torch.device("cuda", torch.cuda.current_device())
+           if dist.get_backend(group) == "nccl" else torch.device("cpu"))
     per = (B + R - 1) // R
     st = torch.full((per,), -9, dtype=torch.int64, device=dev)
-    st[:nb] = torch.as_tensor(rep.status, dtype=torch.int64)
+    st[:nb] = torch.as_tensor(np.asarray(rep.status), dtype=torch.int64)
     its = torch.full((per,), -9, dtype=torch.int64, device=dev)
-    its[:nb] = torch.as_tensor(rep.iterations_run, dtype=torch.int64)
-    all_st = torch.empty((R, per), dtype=torch.int64, device=dev)
-    all_it = torch.empty((R, per), dtype=torch.int64, device=dev)
+    its[:nb] = torch.as_tensor(np.asarray(rep.iterations_run), dtype=torch.int64)
+    all_st = torch.empty((R * per,), dtype=torch.int64, device=dev)  # flat: gloo needs it
+    all_it = torch.empty((R * per,), dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(all_st, st, group=group)
     dist.all_gather_into_tensor(all_it, its, group=group)
     sts = all_st.cpu().numpy().ravel()

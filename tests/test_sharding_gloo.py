@@ -136,3 +136,62 @@ def test_decide_matches_oracle_semantics():
     assert decide(3, 5, 1e-6, 0.0, True, 1e-7, -1, 1.0) == (True, N.ST_CONVERGED, -1, 3)
     assert decide(3, 5, 0.0, 1e-10, True, 1.0, -1, 1e-11) == (True, N.ST_CONVERGED, -1, 3)
     assert decide(0, 5, 0.0, 1e-10, True, 1.0, -1, nan)[0] is False
+
+
+def _batch_oracle_solve(x0s, n, dt, max_iters, step_tol):
+    """Per-trajectory oracle solves (the CPU stand-in for solve_batch)."""
+    from types import SimpleNamespace
+    from oracle import oracle as O
+    st, its = [], []
+    for x0 in x0s:
+        r = O.solve(6, (10.0, 28.0, 8.0 / 3.0), O.stepper_by_name("rk4"), x0, np.tile(x0, (n, 1)),
+                    dt, max_iters, step_tol=step_tol, abort_nonfinite=True)
+        st.append(r["status"])
+        its.append(r["iters"])
+    return SimpleNamespace(status=np.array(st), iterations_run=np.array(its))
+
+
+BATCH = dict(B=37, n=256, dt=0.01, max_iters=100, step_tol=1e-10)
+
+
+def _batch_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_01465_b200.configs import CONFIGS
+        from paper_2511_01465_b200.sharded import solve_batch_sharded
+        x0s = CONFIGS[3].x0s()[:BATCH["B"]]
+        rep, off, gathered = solve_batch_sharded(
+            None, None, BATCH["dt"], x0s, None,
+            solve_fn=lambda xs: _batch_oracle_solve(xs, BATCH["n"], BATCH["dt"],
+                                                    BATCH["max_iters"], BATCH["step_tol"]))
+        q.put((rank, off, len(rep.status), gathered["status"].tolist(),
+               gathered["iterations_run"].tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_sharded_two_ranks_gloo():
+    """solve_batch_sharded (sharded.py) on two gloo ranks: contiguous uneven
+    slices (19 + 18 of cfg3's first 37 trajectories), no data-path collective,
+    the statuses / iteration counts all-gathered in trajectory order — equal on
+    both ranks and to the unsharded per-trajectory solves (BASELINE stop rule)."""
+    from paper_2511_01465_b200.configs import CONFIGS
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [(r[1], r[2]) for r in res] == [(0, 19), (19, 18)]
+    assert res[0][3] == res[1][3] and res[0][4] == res[1][4]
+    ref = _batch_oracle_solve(CONFIGS[3].x0s()[:BATCH["B"]], BATCH["n"], BATCH["dt"],
+                              BATCH["max_iters"], BATCH["step_tol"])
+    assert res[0][3] == ref.status.tolist()
+    assert res[0][4] == ref.iterations_run.tolist()
