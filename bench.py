@@ -593,7 +593,13 @@ def main():
     if prof_traffic.exists():
         try:
             tr = json.loads(prof_traffic.read_text()).get(args.workload)
-            if tr:
+            if isinstance(tr, dict):  # per pass of the dominant kernel (ncu)
+                roof["traffic"] = tr["per_pass_dram_bytes"]
+                roof["traffic_unit"] = "DRAM bytes per Newton pass (one chain_pass launch)"
+                roof["traffic_vs_algorithmic"] = round(
+                    tr["per_pass_dram_bytes"] / tr["per_pass_algorithmic_bytes"], 4)
+                roof["traffic_source"] = tr["source"]
+            elif tr:
                 roof["traffic"] = tr
         except ValueError:
             pass
