@@ -48,9 +48,10 @@ struct ChainCfg {
     static constexpr int NCW = 7;                 // compute warps (+ control: 8 warps, 255 regs)
     static constexpr int NCT = NCW * 32;
     static constexpr int NT = NCT + 32;           // + control warp
-    static constexpr int ITEMS = D <= 2 ? 4 : 2;  // consecutive steps per thread
+    static constexpr int ITEMS = D <= 2 ? 6 : 2;  // consecutive steps per thread
     static constexpr int T = NCT * ITEMS;         // steps per tile
-    static constexpr int SL = 4;                  // parked tiles (build i, apply i-3)
+    static constexpr int LAG = D <= 2 ? 2 : 3;    // tile i-LAG is applied in iteration i
+    static constexpr int SL = LAG + 1;            // parked tiles
     static constexpr int E = D * D + D;
     static constexpr int NP = D <= 2 ? 2 : 1;     // explicit steps built together
 };
@@ -115,11 +116,12 @@ template <int D, int ITEMS>
 __device__ __forceinline__ void rows_issue(const double* X, const double* x0, long long N,
                                           long long r0, int lane, double (&rw)[(ITEMS + 1) * D]) {
     if (r0 >= N) return;
-    if constexpr (D == 2 && ITEMS == 4) {
+    if constexpr (D == 2 && ITEMS % 2 == 0) {
         if (r0 + ITEMS <= N) {
             const double* src = X + r0 * 2;
-            ld256_nc(src, rw[2], rw[3], rw[4], rw[5]);
-            ld256_nc(src + 4, rw[6], rw[7], rw[8], rw[9]);
+#pragma unroll
+            for (int q = 0; q < ITEMS / 2; q++)
+                ld256_nc(src + 4 * q, rw[2 + 4 * q], rw[3 + 4 * q], rw[4 + 4 * q], rw[5 + 4 * q]);
             if (lane == 0) {
                 if (r0 == 0) {
                     rw[0] = x0[0];
@@ -145,9 +147,9 @@ __device__ __forceinline__ void rows_issue(const double* X, const double* x0, lo
 template <int D, int ITEMS>
 __device__ __forceinline__ void rows_halo(long long N, long long r0, int lane,
                                           double (&rw)[(ITEMS + 1) * D]) {
-    if constexpr (D == 2 && ITEMS == 4) {
-        const double h0 = __shfl_up_sync(FULL, rw[8], 1);
-        const double h1 = __shfl_up_sync(FULL, rw[9], 1);
+    if constexpr (D == 2 && ITEMS % 2 == 0) {
+        const double h0 = __shfl_up_sync(FULL, rw[2 * ITEMS], 1);
+        const double h1 = __shfl_up_sync(FULL, rw[2 * ITEMS + 1], 1);
         if (lane > 0 && r0 + ITEMS <= N) {
             rw[0] = h0;
             rw[1] = h1;
@@ -199,6 +201,7 @@ chain_pass_kernel(const ChainParams cp, const int it) {
     constexpr int D = P::D;
     using C = ChainCfg<D>;
     constexpr int NCW = C::NCW, NCT = C::NCT, ITEMS = C::ITEMS, T = C::T, SL = C::SL;
+    constexpr int LAG = C::LAG;
     constexpr int E = C::E;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ChainShared<D>& sm = *reinterpret_cast<ChainShared<D>*>(smem_raw);
@@ -327,99 +330,129 @@ chain_pass_kernel(const ChainParams cp, const int it) {
             t = __shfl_sync(FULL, t, 0);
             return (long long)t < ntiles ? (long long)t : -1;
         };
-        long long tm3 = -1, tm2 = -1, tm1 = -1, ti = claim();
-        long long ti1 = ti >= 0 ? claim() : -1;
+        // tq[k] = t_{i-k}, k = 0..LAG (rotated each iteration); ti1, ti2 ahead
+        long long tq[LAG + 1];
+#pragma unroll
+        for (int k = 1; k <= LAG; k++) tq[k] = -1;
+        tq[0] = claim();
+        long long ti1 = tq[0] >= 0 ? claim() : -1;
         long long ti2 = ti1 >= 0 ? claim() : -1;
         if (lane == 0) {
-            sm.tile[0] = ti;
+            sm.tile[0] = tq[0];
             sm.tile[1] = ti1;
         }
         __syncwarp();
         named_arrive<CB_CARRY, NCT + 32>();  // compute iteration 0's hand-off
         unsigned pend = 0;  // in-flight claim of t_{i+3} (lane 0)
         if (lane == 0 && ti2 >= 0) pend = atomicAdd(p.ctr + it, 1u);
-        Chunk pch{0.0, 0ull};  // in-flight prefix of t_{i-2}-1 (lanes < D)
+        Chunk pch{0.0, 0ull};  // in-flight prefix of t_{i+1-LAG}-1 (lanes < D)
         for (int i = 0;; i++) {
-            // compute runs iteration i iff one of t_i .. t_{i-3} exists
-            if (ti < 0 && tm1 < 0 && tm2 < 0 && tm3 < 0) break;
+            // compute runs iteration i iff one of t_i .. t_{i-LAG} exists
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k <= LAG; k++) any |= tq[k] >= 0;
+            if (!any) break;
+            // the prefix this iteration hands over (u-1, u = t_{i+1-LAG}):
+            // loaded now, it lands while the compute warps build t_i
+            {
+                const long long u = tq[LAG - 1];
+                if (u > 0 && lane < D) pch = ld_chunk(&recP[(u - 1) * D + lane]);
+            }
             named_sync2<CB_BUILT, NCT + 32>(i & 1);
-            // does compute run iteration i+1 (t_{i+1} .. t_{i-2})?
-            const bool next = ti1 >= 0 || ti >= 0 || tm1 >= 0 || tm2 >= 0;
-            if (next) {
-                const int nb = (i + 1) & 1;
-                // (2) incoming state of t_{i-2}: the inclusive prefix of t_{i-2}-1
-                if (tm2 >= 0) {
-                    double zz = 0.0;
-                    int zh = 0;
-                    if (tm2 > 0) {
-                        zh = 1;
-                        int spins = 0;
-                        while (true) {
-                            const bool okk = (lane >= D) || pch.tag == tagP;
-                            if (__all_sync(FULL, okk)) break;
-                            if (++spins > 2) __nanosleep(32);
-                            if (lane < D) pch = ld_chunk(&recP[(tm2 - 1) * D + lane]);
+            auto handoff = [&]() {
+                // does compute run iteration i+1 (t_{i+1} .. t_{i+1-LAG})?
+                bool next = ti1 >= 0;
+#pragma unroll
+                for (int k = 0; k < LAG; k++) next |= tq[k] >= 0;
+                if (next) {
+                    const int nb = (i + 1) & 1;
+                    // (2) incoming state of u = t_{i+1-LAG} (applied in compute
+                    //     iteration i+1): the inclusive prefix of u-1
+                    const long long u = tq[LAG - 1];
+                    if (u >= 0) {
+                        double zz = 0.0;
+                        int zh = 0;
+                        if (u > 0) {
+                            zh = 1;
+                            int spins = 0;
+                            while (true) {
+                                const bool okk = (lane >= D) || pch.tag == tagP;
+                                if (__all_sync(FULL, okk)) break;
+                                if (++spins > 2) __nanosleep(32);
+                                if (lane < D) pch = ld_chunk(&recP[(u - 1) * D + lane]);
+                            }
+                            zz = pch.v;
                         }
-                        zz = pch.v;
+                        if (lane < D) sm.z[nb][lane] = zz;
+                        if (lane == 0) {
+                            sm.zhas[nb] = zh;
+                            CHAIN_TRACE(u, 4, chain_now());
+                        }
                     }
-                    if (lane < D) sm.z[nb][lane] = zz;
+                    // (3) t_{i+2}, whose rows compute prefetches in iteration i+1
+                    if (lane == 0) sm.tile[(i + 2) & 3] = ti2;
+                    __syncwarp();
+                    named_arrive2<CB_CARRY, NCT + 32>(nb);
+                }
+            };
+            auto publish = [&]() {
+                // (1b) tile aggregate of t_i from the warp totals; publish it (the
+                //      compute warps are already past the hand-off above)
+                const long long ti = tq[0];
+                if (ti >= 0) {
+                    const int pb = i & 1;
+                    Elem<D> a;
+                    bool has = false;
+                    if (lane < NCW) {
+                        has = sm.wthas[pb][lane] != 0;
+#pragma unroll
+                        for (int k = 0; k < D * D; k++) a.F[k] = sm.wt[pb][lane][k];
+#pragma unroll
+                        for (int k = 0; k < D; k++) a.c[k] = sm.wt[pb][lane][D * D + k];
+                    } else {
+                        set_identity<D>(a);
+                    }
+                    warp_inclusive_scan<D>(a, has, lane);
+                    Elem<D> ex;
+                    shfl_up_elem<D>(a, ex, 1);
+                    const bool exhas = __shfl_up_sync(FULL, has, 1) && lane > 0;
+                    const int s = i % SL;
+                    if (lane < NCW) {
+                        sm.wexhas[s][lane] = exhas ? 1 : 0;
+#pragma unroll
+                        for (int k = 0; k < D * D; k++) sm.wex[s][lane][k] = ex.F[k];
+#pragma unroll
+                        for (int k = 0; k < D; k++) sm.wex[s][lane][D * D + k] = ex.c[k];
+                    }
+                    // lane NCW-1 holds the tile aggregate; lanes 0..E-1 publish it
+                    double v = 0.0;
+#pragma unroll
+                    for (int k = 0; k < D * D; k++) {
+                        const double o = __shfl_sync(FULL, a.F[k], NCW - 1);
+                        if (lane == k) v = o;
+                    }
+#pragma unroll
+                    for (int k = 0; k < D; k++) {
+                        const double o = __shfl_sync(FULL, a.c[k], NCW - 1);
+                        if (lane == D * D + k) v = o;
+                    }
+                    if (lane < E) st_chunk(&cp.recA[ti * E + lane], v, tagA);
                     if (lane == 0) {
-                        sm.zhas[nb] = zh;
-                        CHAIN_TRACE(tm2, 4, chain_now());
+                        CHAIN_TRACE(ti, 2, chain_now());
+                        CHAIN_TRACE(ti, 6, (unsigned long long)blockIdx.x);
                     }
                 }
-                // (3) t_{i+2}, whose rows compute prefetches in iteration i+1
-                if (lane == 0) sm.tile[(i + 2) & 3] = ti2;
-                __syncwarp();
-                named_arrive2<CB_CARRY, NCT + 32>(nb);
+            };
+            if constexpr (LAG >= 2) {
+                handoff();
+                publish();
+            } else {
+                // LAG 1: the carry is the prefix of this tile's predecessor, so
+                // this tile's aggregate must be out first (else the CTAs would
+                // publish one after another, each waiting for the previous one)
+                publish();
+                handoff();
             }
-            // (1b) tile aggregate of t_i from the warp totals; publish it (the
-            //      compute warps are already past the hand-off above)
-            if (ti >= 0) {
-                const int pb = i & 1;
-                Elem<D> a;
-                bool has = false;
-                if (lane < NCW) {
-                    has = sm.wthas[pb][lane] != 0;
-#pragma unroll
-                    for (int k = 0; k < D * D; k++) a.F[k] = sm.wt[pb][lane][k];
-#pragma unroll
-                    for (int k = 0; k < D; k++) a.c[k] = sm.wt[pb][lane][D * D + k];
-                } else {
-                    set_identity<D>(a);
-                }
-                warp_inclusive_scan<D>(a, has, lane);
-                Elem<D> ex;
-                shfl_up_elem<D>(a, ex, 1);
-                const bool exhas = __shfl_up_sync(FULL, has, 1) && lane > 0;
-                const int s = i % SL;
-                if (lane < NCW) {
-                    sm.wexhas[s][lane] = exhas ? 1 : 0;
-#pragma unroll
-                    for (int k = 0; k < D * D; k++) sm.wex[s][lane][k] = ex.F[k];
-#pragma unroll
-                    for (int k = 0; k < D; k++) sm.wex[s][lane][D * D + k] = ex.c[k];
-                }
-                // lane NCW-1 holds the tile aggregate; lanes 0..E-1 publish it
-                double v = 0.0;
-#pragma unroll
-                for (int k = 0; k < D * D; k++) {
-                    const double o = __shfl_sync(FULL, a.F[k], NCW - 1);
-                    if (lane == k) v = o;
-                }
-#pragma unroll
-                for (int k = 0; k < D; k++) {
-                    const double o = __shfl_sync(FULL, a.c[k], NCW - 1);
-                    if (lane == D * D + k) v = o;
-                }
-                if (lane < E) st_chunk(&cp.recA[ti * E + lane], v, tagA);
-                if (lane == 0) {
-                    CHAIN_TRACE(ti, 2, chain_now());
-                    CHAIN_TRACE(ti, 6, (unsigned long long)blockIdx.x);
-                }
-            }
-            // (4) the prefix the next hand-off needs (t_{i-1}-1)
-            if (tm1 > 0 && lane < D) pch = ld_chunk(&recP[(tm1 - 1) * D + lane]);
             // (5) the claim issued last iteration is t_{i+3}; issue t_{i+4}'s
             long long ti3 = -1;
             if (ti2 >= 0) {
@@ -428,10 +461,9 @@ chain_pass_kernel(const ChainParams cp, const int it) {
                 if (lane == 0 && ti3 >= 0) CHAIN_TRACE(ti3, 0, chain_now());
             }
             if (lane == 0 && ti3 >= 0) pend = atomicAdd(p.ctr + it, 1u);
-            tm3 = tm2;
-            tm2 = tm1;
-            tm1 = ti;
-            ti = ti1;
+#pragma unroll
+            for (int k = LAG; k > 0; k--) tq[k] = tq[k - 1];
+            tq[0] = ti1;
             ti1 = ti2;
             ti2 = ti3;
         }
@@ -439,31 +471,43 @@ chain_pass_kernel(const ChainParams cp, const int it) {
     } else {
         // ------------------------------------------------------------ compute --
         // Iteration i: (after the hand-off barrier) issue the loads of the rows
-        // of t_{i+1} and of the old rows of t_{i-3}, build t_i into slot
-        // i % SL, then apply t_{i-3} with the incoming state the control warp
-        // handed over in iteration i-1.  Loads are issued right after a
+        // of t_{i+1} and of the old rows of t_{i-LAG}, build t_i into slot
+        // i % SL, then apply t_{i-LAG} with the incoming state the control
+        // warp handed over in iteration i-1.  Loads are issued right after a
         // barrier and consumed before the next one (a barrier waits for the
         // thread's outstanding loads).
         named_sync2<CB_CARRY, NCT + 32>(0);
-        long long tm3 = -1, tm2 = -1, tm1 = -1, ti = sm.tile[0], ti1 = sm.tile[1];
+        long long tq[LAG + 1];  // tq[k] = t_{i-k}
+#pragma unroll
+        for (int k = 1; k <= LAG; k++) tq[k] = -1;
+        tq[0] = sm.tile[0];
+        const long long ti1 = sm.tile[1];
         double rw[(ITEMS + 1) * D];   // rows of t_i (row before the thread's first step first)
         double rwn[(ITEMS + 1) * D];  // rows of t_{i+1}, loading
-        double xo[ITEMS * D];         // old rows of t_{i-3}, loading
-        if (ti >= 0) rows_issue<D, ITEMS>(cur, p.x0, N, ti * T + (long long)tid * ITEMS, lane, rw);
-        // the thread's exclusive prefix (within its warp) in tiles t_i .. t_{i-3}
-        Elem<D> tin0, tin1, tin2, tin3;
-        bool tinh0 = false, tinh1 = false, tinh2 = false, tinh3 = false;
+        double xo[ITEMS * D];         // old rows of t_{i-LAG}, loading
+        if (tq[0] >= 0) rows_issue<D, ITEMS>(cur, p.x0, N, tq[0] * T + (long long)tid * ITEMS, lane, rw);
+        // the thread's exclusive prefix (within its warp) in tiles t_i .. t_{i-LAG}
+        Elem<D> tin[LAG + 1];
+        bool tinh[LAG + 1];
+#pragma unroll
+        for (int k = 0; k <= LAG; k++) tinh[k] = false;
         for (int i = 0;; i++) {
-            if (ti < 0 && tm1 < 0 && tm2 < 0 && tm3 < 0) break;
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k <= LAG; k++) any |= tq[k] >= 0;
+            if (!any) break;
+            const long long ti = tq[0], ta = tq[LAG];  // built / applied this iteration
             if (i > 0) named_sync2<CB_CARRY, NCT + 32>(i & 1);
             const long long tn = i > 0 ? sm.tile[(i + 1) & 3] : ti1;  // t_{i+1}
-            // ---- loads: rows of t_{i+1}, old rows of t_{i-3}
+            // ---- loads: rows of t_{i+1}, old rows of t_{i-LAG}
             if (tn >= 0) rows_issue<D, ITEMS>(cur, p.x0, N, tn * T + (long long)tid * ITEMS, lane, rwn);
-            if (tm3 >= 0) {
-                const long long r0 = tm3 * T + (long long)tid * ITEMS;
-                if (D == 2 && ITEMS == 4 && r0 + ITEMS <= N) {
-                    ld256_nc(cur + r0 * 2, xo[0], xo[1], xo[2], xo[3]);
-                    ld256_nc(cur + r0 * 2 + 4, xo[4], xo[5], xo[6], xo[7]);
+            if (ta >= 0) {
+                const long long r0 = ta * T + (long long)tid * ITEMS;
+                if (D == 2 && ITEMS % 2 == 0 && r0 + ITEMS <= N) {
+#pragma unroll
+                    for (int q = 0; q < ITEMS / 2; q++)
+                        ld256_nc(cur + r0 * 2 + 4 * q, xo[4 * q], xo[4 * q + 1], xo[4 * q + 2],
+                                 xo[4 * q + 3]);
                 } else {
 #pragma unroll
                     for (int q = 0; q < ITEMS; q++)
@@ -474,7 +518,7 @@ chain_pass_kernel(const ChainParams cp, const int it) {
             }
             // ---- build t_i
             const int s = i % SL;
-            tinh0 = false;
+            tinh[0] = false;
             if (ti >= 0) {
                 if (tid == 0) CHAIN_TRACE(ti, 1, chain_now());
                 const long long r0 = ti * T + (long long)tid * ITEMS;
@@ -540,8 +584,8 @@ chain_pass_kernel(const ChainParams cp, const int it) {
                     if (!has) set_identity<D>(agg);
                     warp_inclusive_scan<D>(agg, ih, lane);
                 }
-                shfl_up_elem<D>(agg, tin0, 1);
-                tinh0 = __shfl_up_sync(FULL, ih, 1) && lane > 0;
+                shfl_up_elem<D>(agg, tin[0], 1);
+                tinh[0] = __shfl_up_sync(FULL, ih, 1) && lane > 0;
                 if (lane == 31) {
                     const int pb = i & 1;
 #pragma unroll
@@ -551,9 +595,9 @@ chain_pass_kernel(const ChainParams cp, const int it) {
                     sm.wthas[pb][w] = ih ? 1 : 0;
                 }
             }
-            // ---- apply t_{i-3}: dx_k = F_k dx_{k-1} + c_k from its incoming state
-            if (tm3 >= 0) {
-                const int s3 = (i + 1) % SL;  // == (i - 3) % SL
+            // ---- apply t_{i-LAG}: dx_k = F_k dx_{k-1} + c_k from its incoming state
+            if (ta >= 0) {
+                const int s3 = (i + 1) % SL;  // == (i - LAG) % SL (SL = LAG + 1)
                 const int pb = i & 1;
                 double z[D];
                 bool zh = sm.zhas[pb] != 0;
@@ -577,8 +621,8 @@ chain_pass_kernel(const ChainParams cp, const int it) {
                     for (int k = 0; k < D; k++) e.c[k] = sm.wex[s3][w][D * D + k];
                     through(e, true);
                 }
-                through(tin3, tinh3);
-                const long long r0 = tm3 * T + (long long)tid * ITEMS;
+                through(tin[LAG], tinh[LAG]);
+                const long long r0 = ta * T + (long long)tid * ITEMS;
                 double xn[ITEMS * D];
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++) {
@@ -624,21 +668,18 @@ chain_pass_kernel(const ChainParams cp, const int it) {
 #pragma unroll
                             for (int k = 0; k < D; k++) dst[q * D + k] = xn[q * D + k];
                 }
-                if (tid == 0) CHAIN_TRACE(tm3, 5, chain_now());
+                if (tid == 0) CHAIN_TRACE(ta, 5, chain_now());
             }
             named_arrive2<CB_BUILT, NCT + 32>(i & 1);
 #pragma unroll
             for (int j = 0; j < (ITEMS + 1) * D; j++) rw[j] = rwn[j];
-            tin3 = tin2;
-            tinh3 = tinh2;
-            tin2 = tin1;
-            tinh2 = tinh1;
-            tin1 = tin0;
-            tinh1 = tinh0;
-            tm3 = tm2;
-            tm2 = tm1;
-            tm1 = ti;
-            ti = tn;
+#pragma unroll
+            for (int k = LAG; k > 0; k--) {
+                tin[k] = tin[k - 1];
+                tinh[k] = tinh[k - 1];
+                tq[k] = tq[k - 1];
+            }
+            tq[0] = tn;
         }
     }
 
