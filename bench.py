@@ -613,6 +613,15 @@ def main():
                 opath = route_of(ow)
                 oms = statistics.median(od)
                 ov = ow.B * ow.n * args.iters / (oms * 1e-3)
+                # the same solve through solve_batch with host numpy buffers
+                ed, eh2d, ed2h, enote = e2e_steps(ow, 5, 3)
+                ems = statistics.median(ed)
+                ocpu = None
+                if not args.no_cpu:
+                    # bounded CPU sample (cfg4: ~17 s per iteration at the full
+                    # N on the host, so its sample runs N = 1024, per step)
+                    ocpu = cpu_baseline(ocid, args.iters, min(3.0, args.cpu_seconds),
+                                        n_override=1024 if ocid == 4 else None)
                 ow.set_mode(fixed=False)
                 sd, _ = time_steps(ow, 3, 1, flush)
                 oi, os_, ox = ow.outcome()
@@ -621,6 +630,12 @@ def main():
                     "path": opath,
                     "roofline": roofline_for(ocid, ow.n, ow.B, args.iters, oms, hbm, hbm_src,
                                              fp64, fp64_src),
+                    "e2e": {"value": ow.B * ow.n * args.iters / (ems * 1e-3),
+                            "unit": "Newton time-steps/s", "ms": round(ems, 4),
+                            "h2d_bytes_per_step": eh2d, "d2h_bytes_per_step": ed2h,
+                            "guess": enote,
+                            "api": "solve_batch(numpy x0s, numpy guess) -> numpy"},
+                    "cpu_baseline": ocpu,
                     "stop_rule": {"ms": round(statistics.median(sd), 4),
                                   "status_counts": {names.get(int(k), str(k)): int(v) for k, v in
                                                     zip(*np.unique(os_, return_counts=True))},

@@ -79,8 +79,9 @@ struct ChainParams {
     int* stop;         // set by the deciding CTA
     int* final_alt;    // final iterate lives in Xalt
     double* step_prev; // max|dx| of the previous update (for the step rule)
-    unsigned long long* trace;  // diagnostics (ODX_CHAIN_TRACE): [tile][8] stamps of one pass
+    unsigned long long* trace;  // diagnostics (ODX_CHAIN_TRACE): [tile][16] stamps of one pass
     int trace_it;
+    int knob;  // experiment switches (ODX_CHAIN_KNOB), 0 = product
 };
 
 __device__ __forceinline__ unsigned long long chain_now() {
@@ -90,7 +91,7 @@ __device__ __forceinline__ unsigned long long chain_now() {
 }
 #define CHAIN_TRACE(t_, k_, v_)                                           \
     do {                                                                  \
-        if (cp.trace && it == cp.trace_it) cp.trace[(t_) * 8 + (k_)] = (v_); \
+        if (cp.trace && it == cp.trace_it) cp.trace[(t_) * 16 + (k_)] = (v_); \
     } while (0)
 
 enum : uint32_t { CB_BUILT = 1, CB_CARRY = 3, CB_CW = 5 };
@@ -498,6 +499,7 @@ chain_pass_kernel(const ChainParams cp, const int it) {
             if (!any) break;
             const long long ti = tq[0], ta = tq[LAG];  // built / applied this iteration
             if (i > 0) named_sync2<CB_CARRY, NCT + 32>(i & 1);
+            if (ti >= 0 && tid == 0) CHAIN_TRACE(ti, 8, chain_now());
             const long long tn = i > 0 ? sm.tile[(i + 1) & 3] : ti1;  // t_{i+1}
             // ---- loads: rows of t_{i+1}, old rows of t_{i-LAG}
             if (tn >= 0) rows_issue<D, ITEMS>(cur, p.x0, N, tn * T + (long long)tid * ITEMS, lane, rwn);
@@ -576,6 +578,8 @@ chain_pass_kernel(const ChainParams cp, const int it) {
                 }
                 // warp scan of the thread folds: exclusive prefix per thread,
                 // warp total to the control warp
+                if (tid == 0) CHAIN_TRACE(ti, 9, chain_now());
+                if (tid == 96) CHAIN_TRACE(ti, 12, chain_now());
                 bool ih = has;
                 if (full) {
                     warp_inclusive_scan_full<D>(agg, lane);
@@ -594,6 +598,7 @@ chain_pass_kernel(const ChainParams cp, const int it) {
                     for (int k = 0; k < D; k++) sm.wt[pb][w][D * D + k] = agg.c[k];
                     sm.wthas[pb][w] = ih ? 1 : 0;
                 }
+                if (tid == 0) CHAIN_TRACE(ti, 10, chain_now());
             }
             // ---- apply t_{i-LAG}: dx_k = F_k dx_{k-1} + c_k from its incoming state
             if (ta >= 0) {
@@ -670,6 +675,8 @@ chain_pass_kernel(const ChainParams cp, const int it) {
                 }
                 if (tid == 0) CHAIN_TRACE(ta, 5, chain_now());
             }
+            if (ti >= 0 && tid == 0) CHAIN_TRACE(ti, 11, chain_now());
+            if (ti >= 0 && tid == 96) CHAIN_TRACE(ti, 13, chain_now());
             named_arrive2<CB_BUILT, NCT + 32>(i & 1);
 #pragma unroll
             for (int j = 0; j < (ITEMS + 1) * D; j++) rw[j] = rwn[j];
@@ -747,99 +754,22 @@ template <int D>
 struct ChainLayout {
     size_t red, ctr, done, flags, recA, recP, zero_end, Xalt, total;
     long long ntiles;
-    ChainLayout(long long N, int max_iters) {
+    ChainLayout(long long N, int max_iters, int T) {
         using C = ChainCfg<D>;
-        ntiles = (N + C::T - 1) / C::T;
+        ntiles = (N + T - 1) / T;
         size_t off = 0;
         auto at = [&](size_t bytes) { off = align_up(off, 256); size_t o = off; off += bytes; return o; };
         red = at(4 * ((size_t)max_iters + 1) * 8);  // first: init_ws sets its bad slots
         ctr = at(((size_t)max_iters + 1) * 4);
         done = at(((size_t)max_iters + 1) * 4);
         flags = at(4 * 8);  // stop, final_alt, step_prev
-        recA = at((size_t)ntiles * C::E * sizeof(Chunk));
-        recP = at((size_t)ntiles * D * sizeof(Chunk));
+        const size_t nt32 = ((size_t)ntiles + 31) / 32 * 32;  // (solve_chain2.cuh: 32-tile blocks)
+        recA = at(nt32 * C::E * sizeof(Chunk));
+        recP = at(nt32 * D * sizeof(Chunk));
         zero_end = off;
         Xalt = at((size_t)N * D * 8);
         total = off + 256;
     }
 };
-
-template <class P, int KIND, int S>
-int chain_solve(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
-                size_t* need) {
-    constexpr int D = P::D;
-    using C = ChainCfg<D>;
-    const ChainLayout<D> lay(p.N, p.max_iters);
-    if (query) {
-        *need = lay.total;
-        return ODX_OK;
-    }
-    if (!ws || ws_bytes < lay.total) return fail(ODX_EWORKSPACE, "workspace too small");
-    if (reinterpret_cast<uintptr_t>(p.X) & 15) return fail(ODX_EINVAL, "X must be 16-byte aligned");
-    char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(ws), 256));
-    ChainParams cp;
-    cp.sp = p;
-    cp.sp.red = reinterpret_cast<unsigned long long*>(base + lay.red);
-    cp.sp.ctr = reinterpret_cast<uint32_t*>(base + lay.ctr);
-    cp.sp.Xalt = reinterpret_cast<double*>(base + lay.Xalt);
-    cp.sp.ntiles = lay.ntiles;
-    cp.done = reinterpret_cast<unsigned*>(base + lay.done);
-    cp.stop = reinterpret_cast<int*>(base + lay.flags);
-    cp.final_alt = cp.stop + 1;
-    cp.step_prev = reinterpret_cast<double*>(base + lay.flags + 8);
-    cp.recA = reinterpret_cast<Chunk*>(base + lay.recA);
-    cp.recP = reinterpret_cast<Chunk*>(base + lay.recP);
-    init_ws(base, lay.zero_end, p.max_iters + 1, st);  // red first: bad slots = ~0
-    cp.trace = nullptr;
-    cp.trace_it = 1;
-    static unsigned long long* tbuf = nullptr;
-    static size_t tbytes = 0;
-    const char* tpath = getenv("ODX_CHAIN_TRACE");
-    if (tpath) {
-        const size_t need = (size_t)lay.ntiles * 8 * 8;
-        if (tbytes < need) {
-            if (tbuf) cudaFree(tbuf);
-            ODX_CUDA(cudaMalloc(&tbuf, need));
-            tbytes = need;
-        }
-        ODX_CUDA(cudaMemsetAsync(tbuf, 0, need, st));
-        cp.trace = tbuf;
-    }
-    auto kern = chain_pass_kernel<P, KIND, S>;
-    const size_t smem = sizeof(ChainShared<D>);
-    int per_sm = 0;
-    if (int rc = kernel_occupancy((const void*)kern, C::NT, smem, &per_sm)) return rc;
-    if (per_sm < 1) return fail(ODX_ECUDA, "chain kernel cannot be resident");
-    // one CTA per SM, all co-resident (the scanner in CTA 0 must run alongside
-    // every compute CTA)
-    long long grid = (long long)num_sms();
-    if (grid > lay.ntiles + 1) grid = lay.ntiles + 1;  // CTA 0 scans
-    if (grid < 2) grid = 2;
-    if (getenv("ODX_VERBOSE"))
-        fprintf(stderr, "chain_solve: T=%d smem=%zu per_sm=%d grid=%lld ntiles=%lld\n", C::T, smem,
-                per_sm, grid, lay.ntiles);
-    for (int it = 0; it <= p.max_iters; it++) {
-        int itv = it;
-        void* args[] = {&cp, &itv};
-        ODX_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)grid), dim3(C::NT), args,
-                                             smem, st));
-    }
-    chain_finish_kernel<D><<<2 * num_sms(), 256, 0, st>>>(p.X, cp.sp.Xalt, p.N, cp.final_alt);
-    ODX_CUDA(cudaGetLastError());
-    if (tpath) {  // diagnostics only: synchronous dump of pass 1's stamps
-        const size_t need = (size_t)lay.ntiles * 8 * 8;
-        unsigned long long* h = (unsigned long long*)malloc(need);
-        ODX_CUDA(cudaStreamSynchronize(st));
-        ODX_CUDA(cudaMemcpy(h, tbuf, need, cudaMemcpyDeviceToHost));
-        if (FILE* f = fopen(tpath, "wb")) {
-            fwrite(h, 1, need, f);
-            fclose(f);
-        }
-        free(h);
-    }
-    count_launch(p.max_iters + 3);  // init_ws + passes + finish
-    set_route("chain_pass_kernel (single pass per iteration: x read, x_new written; scanner CTA)");
-    return ODX_OK;
-}
 
 }  // namespace odx

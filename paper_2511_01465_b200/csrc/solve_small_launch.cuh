@@ -12,6 +12,7 @@
 #include "shard_tiled.cuh"
 #include "solve_ws.cuh"
 #include "solve_chain.cuh"
+#include "solve_chain2.cuh"
 
 namespace odx {
 

@@ -2,7 +2,9 @@
 
 The route is chosen once per process from the environment
 (solve_small_launch.cuh), so each case runs in a subprocess:
-  default              single-pass chained kernel (solve_chain.cuh), d <= 3
+  default              single-pass chained kernel (solve_chain2.cuh: two 4-warp groups per
+                       CTA), d <= 3
+  ODX_CHAIN_V=1        its first cut (solve_chain.cuh: 7 compute warps + control warp)
   ODX_CHAIN=0          fused tiled passes (shard_tiled.cuh: fused_tiled_solve)
   + ODX_FUSED_TILED=0  streaming warp-specialised kernel (solve_ws.cuh)
   + ODX_TILED=1        two-pass tiled kernels (solve_tiled.cuh)
@@ -58,7 +60,7 @@ print(json.dumps(dict(err=err, hrel=hrel, iters=rep.iterations_run, ref_iters=re
 '''
 
 
-@pytest.mark.parametrize("route", ["chain", "fused_tiled", "ws", "tiled"])
+@pytest.mark.parametrize("route", ["chain", "chain_v1", "fused_tiled", "ws", "tiled"])
 @pytest.mark.parametrize("case", [("vdp_rk4", 1 << 21, 1e-3, 5), ("vdp_be", 600000, 1e-4, 4),
                                   ("lorenz_rk4", 500001, 1e-5, 4)])
 def test_long_trajectory_routes(case, route):
@@ -66,9 +68,12 @@ def test_long_trajectory_routes(case, route):
     env.pop("ODX_FUSED_TILED", None)
     env.pop("ODX_TILED", None)
     env.pop("ODX_CHAIN", None)
-    if route != "chain":
+    env.pop("ODX_CHAIN_V", None)
+    if route == "chain_v1":
+        env["ODX_CHAIN_V"] = "1"
+    elif route != "chain":
         env["ODX_CHAIN"] = "0"
-    if route not in ("chain", "fused_tiled"):
+    if route not in ("chain", "chain_v1", "fused_tiled"):
         env["ODX_FUSED_TILED"] = "0"
     if route == "tiled":
         env["ODX_TILED"] = "1"

@@ -1,6 +1,9 @@
 """Summarise an ODX_CHAIN_TRACE dump (solve_chain.cuh): per-tile stamps of pass 1
    0 claimed  1 build start  2 A published  3 P published (scanner)
-   4 carry obtained (control)  5 applied  6 CTA  7 scanner ready-run length
+   4 carry obtained (control)  5 applied  6 CTA  7 scanner warp
+   8 iteration top (after the hand-off barrier)  9 build loop done  10 warp scan done
+   11 iteration end (after the apply)  12 / 13 = 9 / 11 on warp 3 (shares its scheduler
+   with the control warp)
 
     ODX_CHAIN_TRACE=/tmp/tr.bin python tools/cfg5_time.py ... ; python tools/chain_trace.py /tmp/tr.bin
 """
@@ -8,7 +11,7 @@ import sys
 
 import numpy as np
 
-a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 8).astype(np.int64)
+a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 16).astype(np.int64)
 n = a.shape[0]
 t0 = a[:, 0][a[:, 0] > 0].min()
 s = a.copy()
@@ -64,3 +67,44 @@ tm = np.median(Pt)
 a_front = int((s[:, 2] >= 0)[(s[:, 2] <= tm)].sum()) if False else int(((s[:, 2] >= 0) & (s[:, 2] <= tm)).sum())
 p_front = int(((s[:, 3] >= 0) & (s[:, 3] <= tm)).sum())
 print(f"at t={tm / 1e3:.0f} us: {a_front} aggregates published, {p_front} prefixes published")
+
+# compute-side phases of the iteration that builds tile t (thread 0 unless noted)
+okc = ok & (a[:, 8] > 0) & (a[:, 9] > 0) & (a[:, 10] > 0) & (a[:, 11] > 0)
+c = a[okc]
+print("top -> build start (loads issued)", q((c[:, 1] - c[:, 8]) / 1e3))
+print("build loop                       ", q((c[:, 9] - c[:, 1]) / 1e3))
+print("warp scan                        ", q((c[:, 10] - c[:, 9]) / 1e3))
+print("apply                            ", q((c[:, 11] - c[:, 10]) / 1e3))
+print("iteration busy (top -> end)      ", q((c[:, 11] - c[:, 8]) / 1e3))
+okw = okc & (a[:, 12] > 0) & (a[:, 13] > 0)
+c3 = a[okw]
+if c3.shape[0]:  # (solve_chain.cuh's 7 + 1 warp kernel only)
+    print("warp 3: build loop (from w0 start)", q((c3[:, 12] - c3[:, 1]) / 1e3))
+    print("warp 3: iteration end vs warp 0   ", q((c3[:, 13] - c3[:, 11]) / 1e3))
+# barrier wait: next tile's top on the same CTA minus this iteration's end
+waits = []
+for cc in np.unique(cta[okc]):
+    m = okc & (cta == cc)
+    idx = np.argsort(a[m, 8])
+    tops = a[m, 8][idx]
+    ends = a[m, 11][idx]
+    if tops.size > 2:
+        waits.append(tops[1:] - ends[:-1])
+waits = np.concatenate(waits)
+print("end -> next top (barrier wait)   ", q(waits / 1e3))
+
+# scanner windows (solve_chain2.cuh): lane 0's stamps on the window's first tile
+win = (a[:, 12] > 0) & (a[:, 13] > 0) & (a[:, 14] > 0) & (a[:, 3] > 0)
+if win.sum() > 8:
+    ws = a[win]
+    idx = np.nonzero(win)[0]
+    wl = int(np.median(np.diff(idx)))
+    print(f"scanner windows: {win.sum()} of {wl} tiles")
+    lastA = np.array([a[i:i + wl, 2].max() for i in idx])
+    print("window start -> complete (poll)  ", q((ws[:, 13] - ws[:, 12]) / 1e3))
+    print("last A of window -> complete     ", q((ws[:, 13] - lastA) / 1e3))
+    print("complete -> state obtained       ", q((ws[:, 14] - ws[:, 13]) / 1e3))
+    print("state obtained -> P published    ", q((ws[:, 3] - ws[:, 14]) / 1e3))
+    print("polls per window                 ", q(ws[:, 7].astype(float)))
+    st = np.sort(ws[:, 14])
+    print("state hand-off interval          ", q(np.diff(st) / 1e3))
