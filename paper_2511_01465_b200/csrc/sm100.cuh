@@ -105,16 +105,15 @@ __device__ __forceinline__ void st_chunk(Chunk* p, double v, unsigned long long 
         "l"(__double_as_longlong(v)), "l"(tag)
         : "memory");
 }
+// The result is one 128-bit register operand ("q" constraint): unpacking it is
+// register renaming, so nothing waits for the load until a field is first
+// used (with a .b128 temporary inside the asm block the unpacking mov sat
+// right behind the load and made every prefetch synchronous).
 __device__ __forceinline__ Chunk ld_chunk(const Chunk* p) {
-    long long v;
-    unsigned long long t;
-    asm volatile(
-        "{\n\t.reg .b128 t;\n\tld.relaxed.gpu.global.b128 t, [%2];\n\t"
-        "mov.b128 {%0, %1}, t;\n\t}"
-        : "=l"(v), "=l"(t)
-        : "l"(p)
-        : "memory");
-    return Chunk{__longlong_as_double(v), t};
+    unsigned __int128 r;
+    asm volatile("ld.relaxed.gpu.global.b128 %0, [%1];" : "=q"(r) : "l"(p) : "memory");
+    return Chunk{__longlong_as_double((long long)(unsigned long long)r),
+                 (unsigned long long)(r >> 64)};
 }
 // two doubles as one 128-bit relaxed access (payloads whose validity is
 // carried by a separate b128 chunk that holds the tag)

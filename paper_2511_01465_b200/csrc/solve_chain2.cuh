@@ -316,7 +316,6 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
             const long long tn = i > 0 ? sm.tile[g][(i + 1) & 3] : ti1;  // t_{i+1}
             // ---- loads: rows of t_{i+1}, old rows of t_{i-LAG}, its carry
             if (tn >= 0) rows_issue<D, ITEMS>(cur, p.x0, N, tn * T + (long long)tid * ITEMS, lane, rwn);
-            Chunk pch{0.0, 0ull};
             if (ta >= 0) {
                 const long long r0 = ta * T + (long long)tid * ITEMS;
                 if (D == 2 && ITEMS % 2 == 0 && r0 + ITEMS <= N) {
@@ -331,7 +330,6 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
 #pragma unroll
                             for (int k = 0; k < D; k++) xo[q * D + k] = __ldg(cur + (r0 + q) * D + k);
                 }
-                if (ta > 0 && lane < D) pch = ld_chunk(&cp.recP[rec_idx<D>(ta - 1, lane)]);
             }
             // ---- build t_i
             const int s = i % SL;
@@ -428,6 +426,14 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                 }
                 sm.tile[g][(i + 2) & 3] = t2;
             }
+            // the carry of t_{i-LAG}, sampled as late as possible: it lands
+            // while the group waits at its barrier and folds the warp totals.
+            // (Every lane loads, from a clamped address, so that the chunk's
+            // registers are written by the load alone: a conditional load
+            // merges with a default value through moves that wait for it.
+            // Measured: sampled at the top of the iteration instead, without
+            // waiting, 15.3 ms per cfg5 solve against 13.9 ms.)
+            Chunk pch = ld_chunk(&cp.recP[rec_idx<D>(ta > 0 ? ta - 1 : 0, lane < D ? lane : 0)]);
             group_sync();
             // ---- fold the totals of the warps before this one into the
             //      threads' exclusive prefixes; the last warp publishes the
