@@ -91,7 +91,7 @@ __device__ __forceinline__ unsigned long long chain_now() {
 }
 #define CHAIN_TRACE(t_, k_, v_)                                           \
     do {                                                                  \
-        if (cp.trace && it == cp.trace_it) cp.trace[(t_) * 16 + (k_)] = (v_); \
+        if (cp.trace && !(cp.knob & 4) && it == cp.trace_it) cp.trace[(t_) * 16 + (k_)] = (v_); \
     } while (0)
 
 enum : uint32_t { CB_BUILT = 1, CB_CARRY = 3, CB_CW = 5 };

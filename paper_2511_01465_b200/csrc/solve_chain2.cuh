@@ -304,6 +304,7 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
         // the thread's exclusive prefix within its tile, tiles t_i .. t_{i-LAG}
         Elem<D> tin[LAG + 1];
         bool tinh[LAG + 1];
+        unsigned nspin = 0, nlate = 0, napp = 0;  // diagnostics (ODX_CHAIN_KNOB & 4)
 #pragma unroll
         for (int k = 0; k <= LAG; k++) tinh[k] = false;
         for (int i = 0;; i++) {
@@ -505,6 +506,9 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                         if (++spins > 2) __nanosleep(32);
                         if (lane < D) pch = ld_chunk(&cp.recP[rec_idx<D>(ta - 1, lane)]);
                     }
+                    nspin += spins;
+                    nlate += spins ? 1 : 0;
+                    napp++;
 #pragma unroll
                     for (int k = 0; k < D; k++) z[k] = __shfl_sync(FULL, pch.v, k);
                 }
@@ -577,6 +581,12 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
             }
             tq[0] = tn;
         }
+        if (cp.trace && (cp.knob & 4) && it == cp.trace_it && lane == 0) {
+            atomicAdd(cp.trace + 0, (unsigned long long)nspin);
+            atomicAdd(cp.trace + 1, (unsigned long long)nlate);
+            atomicAdd(cp.trace + 2, (unsigned long long)napp);
+        }
+
     }
 
     // ---------------------------------------------- reductions + decision --
