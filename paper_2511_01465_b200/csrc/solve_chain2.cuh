@@ -315,23 +315,6 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
             const long long ti = tq[0], ta = tq[LAG];  // built / applied this iteration
             if (ti >= 0 && tid == 0) CHAIN_TRACE(ti, 8, chain_now());
             const long long tn = i > 0 ? sm.tile[g][(i + 1) & 3] : ti1;  // t_{i+1}
-            // ---- loads: rows of t_{i+1}, old rows of t_{i-LAG}, its carry
-            if (tn >= 0) rows_issue<D, ITEMS>(cur, p.x0, N, tn * T + (long long)tid * ITEMS, lane, rwn);
-            if (ta >= 0) {
-                const long long r0 = ta * T + (long long)tid * ITEMS;
-                if (D == 2 && ITEMS % 2 == 0 && r0 + ITEMS <= N) {
-#pragma unroll
-                    for (int q = 0; q < ITEMS / 2; q++)
-                        ld256_nc(cur + r0 * 2 + 4 * q, xo[4 * q], xo[4 * q + 1], xo[4 * q + 2],
-                                 xo[4 * q + 3]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < ITEMS; q++)
-                        if (r0 + q < N)
-#pragma unroll
-                            for (int k = 0; k < D; k++) xo[q * D + k] = __ldg(cur + (r0 + q) * D + k);
-                }
-            }
             // ---- build t_i
             const int s = i % SL;
             const int pb = i & 1;
@@ -412,6 +395,26 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                     sm.wthas[g][pb][gw] = ih ? 1 : 0;
                 }
                 if (tid == 0) CHAIN_TRACE(ti, 10, chain_now());
+            }
+            // ---- loads: rows of t_{i+1}, old rows of t_{i-LAG}.  Issued AFTER
+            //      the build, so their 52 registers are free while the pairs
+            //      are built (the build's schedule is register-bound); they
+            //      land during the barrier, the fold and the apply
+            if (tn >= 0) rows_issue<D, ITEMS>(cur, p.x0, N, tn * T + (long long)tid * ITEMS, lane, rwn);
+            if (ta >= 0) {
+                const long long r0 = ta * T + (long long)tid * ITEMS;
+                if (D == 2 && ITEMS % 2 == 0 && r0 + ITEMS <= N) {
+#pragma unroll
+                    for (int q = 0; q < ITEMS / 2; q++)
+                        ld256_nc(cur + r0 * 2 + 4 * q, xo[4 * q], xo[4 * q + 1], xo[4 * q + 2],
+                                 xo[4 * q + 3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++)
+                        if (r0 + q < N)
+#pragma unroll
+                            for (int k = 0; k < D; k++) xo[q * D + k] = __ldg(cur + (r0 + q) * D + k);
+                }
             }
             // ---- the claim issued one iteration ago is t_{i+2}; issue t_{i+3}'s
             if (tid == 0) {

@@ -4,9 +4,10 @@ odescan._kernels (/root/reference/pkg/src/odescan/_kernels.py) exposes
 build_explicit (:299-342), build_implicit (:393-464), scan_affine (:116-233),
 max_abs (:84-95) and add_inplace (:98-103) over numpy arrays.  These are the
 same operations on CUDA torch tensors (fp64, C-contiguous), each one call into
-libodescan_b200.so.  solve() does not use them — it runs the fused
-single-pass kernel — they exist for parity bisection and for callers that
-drive their own Newton loop.
+libodescan_b200.so.  solve() does not use them — it runs the fused solve
+kernels (one launch per solve for resident / one-wave trajectories, one launch
+per Newton iteration for long ones) — they exist for parity bisection and for
+callers that drive their own Newton loop.
 """
 
 from __future__ import annotations
