@@ -1,15 +1,21 @@
-// solve_chain2.cuh — the single-pass chained Newton iteration (solve_chain.cuh),
-// re-cut so the phases of a tile overlap on the SM.
+// solve_chain2.cuh — single-pass chained Newton iteration for long trajectories
+// (cfg 5: one trajectory of N = 2^26 steps, d = 2).
 //
-// solve_chain.cuh runs one CTA per SM: seven compute warps walk through build ->
-// warp scan -> hand-off barrier -> apply in lockstep, so the FP64 pipe idles
-// while they scan, wait and apply (trace: build 2.2 us of a 4.5 us tile period).
-// Here each CTA (one per SM, 8 warps, 255 registers per thread) holds TWO
-// independent groups of four warps, each with its own tile stream, its own half
-// of the shared memory and its own named barrier: while one group scans, waits
-// at its barrier, polls its carry or applies, the other one builds (each
-// scheduler holds one warp of each group).  There is no control warp: all
-// eight warps build.
+// One launch per Newton iteration reads X_it once and writes X_it+1 once
+// (16*d bytes per step, SURVEY §8(d)'s algorithmic traffic): the residual,
+// the step-map Jacobian (_kernels.build_explicit :299-342 / build_implicit
+// :393-464), the affine scan (_kernels.scan_affine :116-233) and the update
+// (add_inplace :98-103) all happen while a tile's data is on chip.
+//
+// Each CTA (one per SM, 8 warps, 255 registers per thread) holds independent
+// GROUPS of warps (four groups of two warps for heavy builds, two groups of four
+// otherwise), each with its own tile stream, its own share of the shared memory
+// and its own named barrier: while one group scans, waits at its barrier, polls
+// its carry or applies, the others build (each scheduler holds warps of
+// different groups).  There is no control warp: all eight warps build.  With
+// the warps of a CTA in lockstep (the first cut of this kernel) the FP64 pipe
+// idled through every scan / barrier / apply phase: build 2.2 us of a 4.5 us
+// tile period.
 //
 //   group, iteration i (tile t_i claimed two iterations ahead):
 //     top      issue the loads of the rows of t_{i+1}, of the old rows of
@@ -17,7 +23,7 @@
 //     build    t_i's elements (ITEMS consecutive steps per thread, pairs
 //              interleaved), parked in shared-memory slot i % SL; thread fold;
 //              warp scan; warp total to shared memory
-//     barrier  ONE 128-thread named barrier per tile
+//     barrier  ONE named barrier of the group per tile
 //     compose  every warp folds the totals of the warps before it into its
 //              threads' exclusive prefixes; the last warp publishes the tile
 //              aggregate (E .b128 chunks)
@@ -36,11 +42,21 @@
 
 namespace odx {
 
-template <int D>
+// Warps per group.  Two-warp groups (four per CTA) overlap best when the build
+// is heavy (d = 2, RK3 / RK4 or an implicit step: cfg5 12.8 ms against 13.5 ms
+// with four-warp groups); their 384-step tiles double the scanner's load, and a
+// cheap build (Euler, d = 1) or the small d = 3 tiles would run at the
+// scanner's rate (one hand-off per 32 tiles, ~0.19 us) — those keep four warps.
+template <int D, int KIND, int S>
+constexpr int chain2_group_warps() {
+    return (D == 2 && (KIND == 1 || S >= 3)) ? 2 : 4;
+}
+
+template <int D, int NWV>
 struct Chain2Cfg {
-    static constexpr int NW = 4;   // warps per group (all compute)
+    static constexpr int NW = NWV;      // warps per group (all compute)
     static constexpr int GT = NW * 32;  // threads per group
-    static constexpr int NG = 2;        // groups per CTA
+    static constexpr int NG = 8 / NW;   // groups per CTA
     static constexpr int NT = NG * GT;
     static constexpr int NWS = NG * NW;  // scanner warps (CTA 0)
     static constexpr int ITEMS = D <= 2 ? 6 : 2;  // consecutive steps per thread
@@ -49,22 +65,19 @@ struct Chain2Cfg {
     static constexpr int SL = LAG + 1;            // parked tiles
     static constexpr int E = D * D + D;
     static constexpr int NP = D <= 2 ? 2 : 1;     // explicit steps built together
-#ifndef ODX_CHAIN2_TPL
-#define ODX_CHAIN2_TPL 1
-#endif
-    static constexpr int TPL = ODX_CHAIN2_TPL;    // scanner: tiles per lane
+    static constexpr int TPL = 1;                 // scanner: tiles per lane
     static constexpr int WIN = 32 * TPL;          // scanner: tiles per window
 };
 
-template <int D>
+template <int D, int NWV>
 struct Chain2Shared {
-    using C = Chain2Cfg<D>;
+    using C = Chain2Cfg<D, NWV>;
     double els[C::NG][C::SL][C::E][C::T];  // [group][slot][component][item*GT + thread]
     double wt[C::NG][2][C::NW][C::E];      // warp totals of the tile being built
     int wthas[C::NG][2][C::NW];
     long long tile[C::NG][4];  // claimed tile ids, by i % 4
     double zr[16][D];          // scanner: running state after window j, by j % 16
-    long long zwin;
+    long long ztag[16];        // = j once zr[j % 16] holds the state after window j
     double redd[3][C::NWS];
     unsigned long long redb[C::NWS];
 };
@@ -79,14 +92,14 @@ __device__ __forceinline__ long long rec_idx(long long t, int c) {
 }
 
 template <class P, int KIND, int S>
-__global__ void __launch_bounds__(Chain2Cfg<P::D>::NT, 1)
+__global__ void __launch_bounds__(256, 1)
 chain2_pass_kernel(const ChainParams cp, const int it) {
     constexpr int D = P::D;
-    using C = Chain2Cfg<D>;
+    using C = Chain2Cfg<D, chain2_group_warps<D, KIND, S>()>;
     constexpr int NW = C::NW, GT = C::GT, NWS = C::NWS, ITEMS = C::ITEMS, T = C::T, SL = C::SL;
     constexpr int LAG = C::LAG, E = C::E, TPL = C::TPL, WIN = C::WIN;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Chain2Shared<D>& sm = *reinterpret_cast<Chain2Shared<D>*>(smem_raw);
+    Chain2Shared<D, NW>& sm = *reinterpret_cast<Chain2Shared<D, NW>*>(smem_raw);
     const SolveParams& p = cp.sp;
     if (*(volatile int*)cp.stop) return;
 
@@ -137,8 +150,7 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
         // element 0 has F = 0 (_kernels.py:333-336).
         const Chunk* recA = cp.recA;
         Chunk* recP = cp.recP;
-        volatile long long* zwin = &sm.zwin;
-        if (threadIdx.x == 0) *zwin = -1;
+        if (threadIdx.x < 16) ((volatile long long*)sm.ztag)[threadIdx.x] = -1;
         __syncthreads();
         // (Measured: prefetching a warp's next window while it scans the
         // current one loses 12% — the prefetched copy is always stale, because
@@ -200,14 +212,20 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
             // finished this window); shared memory is accessed with volatile
             // operations and no fence (a membar would also wait for the warp's
             // outstanding global stores): one thread writes the state, then
-            // zwin, and the SM's shared-memory pipe performs a thread's
+            // its tag, and the SM's shared-memory pipe performs a thread's
             // accesses in program order.
             if (lane == lv) {
                 double hz[D], ho[D];
                 if (zh) {
-                    while (*zwin != j - 1) { }
+                    // tag first, state second (performed in that order): a
+                    // probe that sees the tag also has the state, in one
+                    // shared-memory round trip
+                    while (true) {
+                        const long long tg = ((volatile long long*)sm.ztag)[(j - 1) & 15];
 #pragma unroll
-                    for (int k = 0; k < D; k++) hz[k] = ((volatile double*)sm.zr[(j - 1) & 15])[k];
+                        for (int k = 0; k < D; k++) hz[k] = ((volatile double*)sm.zr[(j - 1) & 15])[k];
+                        if (tg == j - 1) break;
+                    }
                     apply<D>(a, hz, ho);
                 } else {
 #pragma unroll
@@ -215,7 +233,7 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                 }
 #pragma unroll
                 for (int k = 0; k < D; k++) ((volatile double*)sm.zr[j & 15])[k] = ho[k];
-                *zwin = j;
+                ((volatile long long*)sm.ztag)[j & 15] = j;
             }
             __syncwarp();
             if (zh) {
@@ -272,7 +290,14 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
     } else {
         // ------------------------------------------------------------ compute --
         auto group_sync = [&]() {
-            if (g == 0) named_sync<1, GT>(); else named_sync<2, GT>();
+            if constexpr (NW == 1) {
+                __syncwarp();
+            } else {
+                if (g == 0) named_sync<1, GT>();
+                else if (g == 1) named_sync<2, GT>();
+                else if (g == 2) named_sync<3, GT>();
+                else named_sync<4, GT>();
+            }
         };
         auto claim_now = [&]() -> long long {
             const unsigned t = atomicAdd(p.ctr + it, 1u);
@@ -643,23 +668,13 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
 
 // The pass kernel of solve_chain2.cuh (two 4-warp CTAs per SM, the default) or
 // the one above (ODX_CHAIN_V=1: one CTA per SM, 7 compute warps + control).
-inline int chain_version() {
-    static const int v = [] {
-        const char* e = getenv("ODX_CHAIN_V");
-        return (e && e[0] == '1') ? 1 : 2;
-    }();
-    return v;
-}
-
 template <class P, int KIND, int S>
 int chain_solve(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
                 size_t* need) {
     constexpr int D = P::D;
-    using C1 = ChainCfg<D>;
-    using C2 = Chain2Cfg<D>;
-    const bool v2 = chain_version() == 2;
-    const int T = v2 ? C2::T : C1::T;
-    const int NT = v2 ? C2::NT : C1::NT;
+    using C2 = Chain2Cfg<D, chain2_group_warps<D, KIND, S>()>;
+    constexpr int T = C2::T;
+    constexpr int NT = C2::NT;
     const ChainLayout<D> lay(p.N, p.max_iters, T);
     if (query) {
         *need = lay.total;
@@ -697,21 +712,19 @@ int chain_solve(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
         ODX_CUDA(cudaMemsetAsync(tbuf, 0, need, st));
         cp.trace = tbuf;
     }
-    const void* kern = v2 ? (const void*)chain2_pass_kernel<P, KIND, S>
-                          : (const void*)chain_pass_kernel<P, KIND, S>;
-    const size_t smem = v2 ? sizeof(Chain2Shared<D>) : sizeof(ChainShared<D>);
+    const void* kern = (const void*)chain2_pass_kernel<P, KIND, S>;
+    const size_t smem = sizeof(Chain2Shared<D, C2::NW>);
     int per_sm = 0;
     if (int rc = kernel_occupancy(kern, NT, smem, &per_sm)) return rc;
     if (per_sm < 1) return fail(ODX_ECUDA, "chain kernel cannot be resident");
     // every CTA co-resident (the scanner in CTA 0 must run alongside every
-    // compute CTA): one CTA per SM, or two of the 4-warp CTAs
-    const int want = 1;
-    long long grid = (long long)num_sms() * (per_sm < want ? per_sm : want);
+    // compute CTA): one CTA per SM
+    long long grid = (long long)num_sms();
     if (grid > lay.ntiles + 1) grid = lay.ntiles + 1;  // CTA 0 scans
     if (grid < 2) grid = 2;
     if (getenv("ODX_VERBOSE"))
-        fprintf(stderr, "chain_solve: v%d T=%d smem=%zu per_sm=%d grid=%lld ntiles=%lld\n",
-                v2 ? 2 : 1, T, smem, per_sm, grid, lay.ntiles);
+        fprintf(stderr, "chain_solve: T=%d (%d-warp groups) smem=%zu per_sm=%d grid=%lld ntiles=%lld\n",
+                T, C2::NW, smem, per_sm, grid, lay.ntiles);
     for (int it = 0; it <= p.max_iters; it++) {
         int itv = it;
         void* args[] = {&cp, &itv};
@@ -731,9 +744,8 @@ int chain_solve(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool
         free(h);
     }
     count_launch(p.max_iters + 3);  // init_ws + passes + finish
-    set_route(v2 ? "chain2_pass_kernel (single pass per iteration: x read, x_new written; two "
-                   "4-warp groups per CTA out of phase, scanner CTA)"
-                 : "chain_pass_kernel (single pass per iteration: x read, x_new written; scanner CTA)");
+    set_route("chain2_pass_kernel (single pass per iteration: x read, x_new written; independent "
+              "warp groups per CTA out of phase, scanner CTA)");
     return ODX_OK;
 }
 

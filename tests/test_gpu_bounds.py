@@ -90,8 +90,6 @@ CASES = [
     ("grid", "vdp_be", 65536 - 77, 1, {}),
     ("chain", "vdp_rk4", 300007, 1, {"ODX_GRID_RESIDENT": "0"}),
     ("chain_d3", "lorenz", 200001, 1, {"ODX_GRID_RESIDENT": "0"}),
-    ("chain_v1", "vdp_rk4", 300007, 1, {"ODX_GRID_RESIDENT": "0", "ODX_CHAIN_V": "1"}),
-    ("chain_v1_d3", "lorenz", 200001, 1, {"ODX_GRID_RESIDENT": "0", "ODX_CHAIN_V": "1"}),
     ("fused", "vdp_rk4", 300007, 1, {"ODX_GRID_RESIDENT": "0", "ODX_CHAIN": "0"}),
     ("ws", "vdp_rk4", 300007, 1, {"ODX_GRID_RESIDENT": "0", "ODX_CHAIN": "0",
                                   "ODX_FUSED_TILED": "0"}),
@@ -104,7 +102,7 @@ CASES = [
 @pytest.mark.parametrize("label,case,n,B,env", CASES, ids=[c[0] for c in CASES])
 def test_no_write_outside_buffers(label, case, n, B, env):
     e = dict(os.environ)
-    for k in ("ODX_GRID_RESIDENT", "ODX_CHAIN", "ODX_CHAIN_V", "ODX_FUSED_TILED", "ODX_TILED"):
+    for k in ("ODX_GRID_RESIDENT", "ODX_CHAIN", "ODX_FUSED_TILED", "ODX_TILED"):
         e.pop(k, None)
     e.update(env)
     out = subprocess.run([sys.executable, "-c", SCRIPT, str(REPO), case, str(n), str(B)], env=e,
@@ -115,7 +113,6 @@ def test_no_write_outside_buffers(label, case, n, B, env):
     assert r["err"] <= 1e-9, r
     expect = {"resident": "resident_solve", "resident_batch": "resident_solve",
               "grid": "grid_resident", "chain": "chain2_pass", "chain_d3": "chain2_pass",
-              "chain_v1": "chain_pass", "chain_v1_d3": "chain_pass",
               "fused": "shard_fused", "ws": "persistent_ws", "tiled": "tiled_build",
               "dense": "dense d=64"}[label]
     assert expect in r["route"], r

@@ -2,9 +2,8 @@
 
 The route is chosen once per process from the environment
 (solve_small_launch.cuh), so each case runs in a subprocess:
-  default              single-pass chained kernel (solve_chain2.cuh: two 4-warp groups per
-                       CTA), d <= 3
-  ODX_CHAIN_V=1        its first cut (solve_chain.cuh: 7 compute warps + control warp)
+  default              single-pass chained kernel (solve_chain2.cuh: independent warp groups
+                       per CTA), d <= 3
   ODX_CHAIN=0          fused tiled passes (shard_tiled.cuh: fused_tiled_solve)
   + ODX_FUSED_TILED=0  streaming warp-specialised kernel (solve_ws.cuh)
   + ODX_TILED=1        two-pass tiled kernels (solve_tiled.cuh)
@@ -32,6 +31,10 @@ if name == "vdp_rk4":
     prob, sname = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt), "rk4"
 elif name == "vdp_be":
     prob, sname = pkg.van_der_pol(mu=10.0, x0=(2.0, 0.0), tf=n * dt), "backward_euler"
+elif name == "vdp_euler":
+    prob, sname = pkg.van_der_pol(mu=1.0, x0=(2.0, 0.0), tf=n * dt), "euler"
+elif name == "logistic_rk4":
+    prob, sname = pkg.logistic(x0=(0.1,), tf=n * dt), "rk4"
 else:
     prob, sname = pkg.lorenz63(x0=(1.0, 1.0, 1.0), tf=n * dt), "rk4"
 nat = prob.native()
@@ -39,6 +42,8 @@ pid, params = nat.problem_id, tuple(nat.params[:nat.n_params])
 ost = O.stepper_by_name(sname)
 if sname == "rk4":
     seq = O.seq_explicit(pid, params, O.RK4_A, O.RK4_B, prob.x0, dt, n)
+elif sname == "euler":
+    seq = O.seq_explicit(pid, params, O.EULER_A, O.EULER_B, prob.x0, dt, n)
 else:
     seq, _ = O.seq_implicit(pid, params, ost.w_prev, ost.w_next, prob.x0, dt, n)
 guess = seq * (1.0 + 1e-3 * np.random.default_rng(3).standard_normal(seq.shape))
@@ -60,7 +65,7 @@ print(json.dumps(dict(err=err, hrel=hrel, iters=rep.iterations_run, ref_iters=re
 '''
 
 
-@pytest.mark.parametrize("route", ["chain", "chain_v1", "fused_tiled", "ws", "tiled"])
+@pytest.mark.parametrize("route", ["chain", "fused_tiled", "ws", "tiled"])
 @pytest.mark.parametrize("case", [("vdp_rk4", 1 << 21, 1e-3, 5), ("vdp_be", 600000, 1e-4, 4),
                                   ("lorenz_rk4", 500001, 1e-5, 4)])
 def test_long_trajectory_routes(case, route):
@@ -68,15 +73,31 @@ def test_long_trajectory_routes(case, route):
     env.pop("ODX_FUSED_TILED", None)
     env.pop("ODX_TILED", None)
     env.pop("ODX_CHAIN", None)
-    env.pop("ODX_CHAIN_V", None)
-    if route == "chain_v1":
-        env["ODX_CHAIN_V"] = "1"
-    elif route != "chain":
+    if route != "chain":
         env["ODX_CHAIN"] = "0"
-    if route not in ("chain", "chain_v1", "fused_tiled"):
+    if route not in ("chain", "fused_tiled"):
         env["ODX_FUSED_TILED"] = "0"
     if route == "tiled":
         env["ODX_TILED"] = "1"
+    name, n, dt, iters = case
+    out = subprocess.run([sys.executable, "-c", SCRIPT, str(REPO), name, str(n), str(dt),
+                          str(iters)], env=env, capture_output=True, text=True, timeout=600,
+                         cwd=str(REPO))
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["fin_equal"]
+    assert r["err"] <= 1e-9, r
+    assert r["hrel"] <= 1e-7, r
+    assert abs(r["iters"] - r["ref_iters"]) <= 1
+
+
+# Cheap builds (explicit Euler, d = 1) run the chain kernel at the scanner's rate — the
+# regime in which the kernel's first cut (control-warp hand-off) could deadlock.
+@pytest.mark.parametrize("case", [("vdp_euler", 3000001, 1e-4, 4), ("logistic_rk4", 3000001, 1e-4, 4)])
+def test_chain_cheap_builds(case):
+    env = dict(os.environ)
+    for k in ("ODX_FUSED_TILED", "ODX_TILED", "ODX_CHAIN"):
+        env.pop(k, None)
     name, n, dt, iters = case
     out = subprocess.run([sys.executable, "-c", SCRIPT, str(REPO), name, str(n), str(dt),
                           str(iters)], env=env, capture_output=True, text=True, timeout=600,
