@@ -59,13 +59,16 @@ struct Chain2Cfg {
     static constexpr int NG = 8 / NW;   // groups per CTA
     static constexpr int NT = NG * GT;
     static constexpr int NWS = NG * NW;  // scanner warps (CTA 0)
-    static constexpr int ITEMS = D <= 2 ? 6 : 2;  // consecutive steps per thread
+    static constexpr int ITEMS = D <= 2 ? 6 : 3;  // consecutive steps per thread
     static constexpr int T = GT * ITEMS;          // steps per tile
-    static constexpr int LAG = D <= 2 ? 2 : 3;    // tile i-LAG is applied in iteration i
+    static constexpr int LAG = 2;                 // tile i-LAG is applied in iteration i
     static constexpr int SL = LAG + 1;            // parked tiles
     static constexpr int E = D * D + D;
     static constexpr int NP = D <= 2 ? 2 : 1;     // explicit steps built together
-    static constexpr int TPL = 1;                 // scanner: tiles per lane
+    // scanner: tiles per lane — 64-tile windows for the 384-step tiles of two-warp
+    // groups, i.e. one hand-off per 24576 steps either way (with 32-tile windows
+    // the hand-off chain took 84% of cfg5's pass; a cheaper build would wait on it)
+    static constexpr int TPL = NWV == 2 ? 2 : 1;
     static constexpr int WIN = 32 * TPL;          // scanner: tiles per window
 };
 
