@@ -75,6 +75,15 @@ __device__ __forceinline__ void rows_issue(const double* X, const double* x0, lo
             return;
         }
     }
+    if constexpr (D == 1 && ITEMS % 2 == 0) {
+        // d = 1: the thread's ITEMS rows as 16-byte pairs (r0 is even)
+        if (r0 + ITEMS <= N) {
+#pragma unroll
+            for (int q = 0; q < ITEMS / 2; q++) ld_row2_nc(X + r0 + 2 * q, rw[1 + 2 * q], rw[2 + 2 * q]);
+            if (lane == 0) rw[0] = (r0 == 0) ? x0[0] : __ldg(X + r0 - 1);
+            return;
+        }
+    }
     if (r0 == 0)
 #pragma unroll
         for (int j = 0; j < D; j++) rw[j] = x0[j];
@@ -96,6 +105,10 @@ __device__ __forceinline__ void rows_halo(long long N, long long r0, int lane,
             rw[0] = h0;
             rw[1] = h1;
         }
+    }
+    if constexpr (D == 1 && ITEMS % 2 == 0) {
+        const double h0 = __shfl_up_sync(FULL, rw[ITEMS], 1);
+        if (lane > 0 && r0 + ITEMS <= N) rw[0] = h0;
     }
 }
 

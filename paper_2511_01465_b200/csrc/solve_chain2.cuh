@@ -436,6 +436,10 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                     for (int q = 0; q < ITEMS / 2; q++)
                         ld256_nc(cur + r0 * 2 + 4 * q, xo[4 * q], xo[4 * q + 1], xo[4 * q + 2],
                                  xo[4 * q + 3]);
+                } else if (D == 1 && ITEMS % 2 == 0 && r0 + ITEMS <= N) {
+#pragma unroll
+                    for (int q = 0; q < ITEMS / 2; q++)
+                        ld_row2_nc(cur + r0 + 2 * q, xo[2 * q], xo[2 * q + 1]);
                 } else {
 #pragma unroll
                     for (int q = 0; q < ITEMS; q++)
@@ -593,11 +597,17 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                             }
                     }
                 } else {
+                    if (D == 1 && ITEMS % 2 == 0 && r0 + ITEMS <= N) {
 #pragma unroll
-                    for (int q = 0; q < ITEMS; q++)
-                        if (r0 + q < N)
+                        for (int q = 0; q < ITEMS / 2; q++)
+                            *reinterpret_cast<double2*>(dst + 2 * q) = make_double2(xn[2 * q], xn[2 * q + 1]);
+                    } else {
 #pragma unroll
-                            for (int k = 0; k < D; k++) dst[q * D + k] = xn[q * D + k];
+                        for (int q = 0; q < ITEMS; q++)
+                            if (r0 + q < N)
+#pragma unroll
+                                for (int k = 0; k < D; k++) dst[q * D + k] = xn[q * D + k];
+                    }
                 }
                 if (tid == 0) CHAIN_TRACE(ta, 5, chain_now());
             }
