@@ -595,7 +595,7 @@ def main():
             tr = json.loads(prof_traffic.read_text()).get(args.workload)
             if isinstance(tr, dict):  # per pass of the dominant kernel (ncu)
                 roof["traffic"] = tr["per_pass_dram_bytes"]
-                roof["traffic_unit"] = "DRAM bytes per Newton pass (one chain_pass launch)"
+                roof["traffic_unit"] = "DRAM bytes per Newton pass (one chain2_pass launch)"
                 roof["traffic_vs_algorithmic"] = round(
                     tr["per_pass_dram_bytes"] / tr["per_pass_algorithmic_bytes"], 4)
                 roof["traffic_source"] = tr["source"]

@@ -679,8 +679,9 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
     }
 }
 
-// The pass kernel of solve_chain2.cuh (two 4-warp CTAs per SM, the default) or
-// the one above (ODX_CHAIN_V=1: one CTA per SM, 7 compute warps + control).
+// Host side: workspace layout, one cooperative launch per Newton iteration (all
+// enqueued up front; passes after the device-side stop return at once), and
+// the finish kernel.
 template <class P, int KIND, int S>
 int chain_solve(SolveParams& p, void* ws, size_t ws_bytes, cudaStream_t st, bool query,
                 size_t* need) {

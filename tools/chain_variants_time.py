@@ -1,5 +1,5 @@
 """Time long single trajectories of several (problem, stepper) pairs on the current
-chain route (ODX_CHAIN_V selects the kernel), device-resident, 5 fixed iterations.
+chain route (solve_chain2.cuh), device-resident, 5 fixed iterations.
 
     python tools/chain_variants_time.py
 """
