@@ -11,6 +11,13 @@
 // buffers; caller buffers that are already page-locked skip the staging copy
 // (DMA to / from them directly).  Calls are serialised by a mutex (the caches
 // are shared).
+//
+// Large batches of resident trajectories (cfg 3: 4096 x 2048 x 3, 201 MB each
+// way) are independent solves, so they run as a pipeline of up to 8 batch
+// chunks, each on its own stream: the host packs chunk k+1 while chunk k is
+// copied in, chunk k-1 is solved and chunk k-2 is copied out (PCIe is full
+// duplex).  The caller's stream forks into the chunk streams after the x0 copy
+// and joins them before the outcome copy, so it still orders the whole call.
 #include <pthread.h>
 
 #include <algorithm>
@@ -49,6 +56,11 @@ struct HostCache {
     size_t in_bytes = 0;
     void* pin_out = nullptr;
     size_t out_bytes = 0;
+    // batch pipeline (large resident batches): one stream + event per chunk
+    static constexpr int MAXC = 8;
+    cudaStream_t cs[MAXC] = {};
+    cudaEvent_t ce[MAXC] = {};
+    cudaEvent_t fork = nullptr;
 };
 
 std::mutex g_host_mu;
@@ -250,6 +262,66 @@ extern "C" int odx_solve_host(const odx_problem* P, const odx_stepper* S, const 
     // the cached staging blocks
     const bool in_pinned = is_pinned(X_guess), out_pinned = is_pinned(X_out);
     std::memcpy(pin, x0, nx0);
+
+    // ---- pipelined batch chunks (independent resident trajectories) ----------
+    static const bool no_pipe = std::getenv("ODX_HOST_PIPELINE") &&
+                                std::getenv("ODX_HOST_PIPELINE")[0] == '0';
+    if (!no_pipe && B >= 64 && nX >= (size_t(32) << 20) && d <= 4 && N <= resident_max_steps((int)d)) {
+        const int K = HostCache::MAXC;
+        const int64_t Bc = (B + K - 1) / K;
+        size_t wsc = odx_solve_workspace_bytes(P, S, Bc, N, C);
+        wsc = al256(wsc < 256 ? 256 : wsc);
+        if ((rc = grow_device(&hc.ws, &hc.wsbytes, wsc * K))) return rc;
+        if (!hc.fork) {
+            ODX_CUDA(cudaEventCreateWithFlags(&hc.fork, cudaEventDisableTiming));
+            for (int k = 0; k < K; k++) {
+                ODX_CUDA(cudaStreamCreateWithFlags(&hc.cs[k], cudaStreamNonBlocking));
+                ODX_CUDA(cudaEventCreateWithFlags(&hc.ce[k], cudaEventDisableTiming));
+            }
+        }
+        char* dout = din + o_out;
+        ODX_CUDA(cudaMemcpyAsync(din, pin, nx0, cudaMemcpyHostToDevice, st));
+        ODX_CUDA(cudaEventRecord(hc.fork, st));
+        const size_t row = (size_t)(N * d) * 8;  // bytes of one trajectory
+        for (int k = 0; k < K; k++) {
+            const int64_t b0 = (int64_t)k * Bc;
+            if (b0 >= B) break;
+            const int64_t bn = (b0 + Bc <= B) ? Bc : B - b0;
+            const size_t off = (size_t)b0 * row, len = (size_t)bn * row;
+            cudaStream_t sk = hc.cs[k];
+            ODX_CUDA(cudaStreamWaitEvent(sk, hc.fork, 0));
+            const char* src = reinterpret_cast<const char*>(X_guess) + off;
+            if (!in_pinned) {
+                CopyPool::get().copy(pin + o_X + off, src, len);
+                src = pin + o_X + off;
+            }
+            ODX_CUDA(cudaMemcpyAsync(din + o_X + off, src, len, cudaMemcpyHostToDevice, sk));
+            rc = odx_solve(P, S, reinterpret_cast<const double*>(din) + b0 * d,
+                           reinterpret_cast<double*>(din + o_X + off), bn, N, dt, C,
+                           reinterpret_cast<double*>(dout) + b0 * H,
+                           reinterpret_cast<double*>(dout + o_sh) + b0 * H,
+                           reinterpret_cast<int32_t*>(dout + o_it) + b0,
+                           reinterpret_cast<int32_t*>(dout + o_st) + b0,
+                           reinterpret_cast<int64_t*>(dout + o_sidx) + b0,
+                           static_cast<char*>(hc.ws) + (size_t)k * wsc, wsc, (void*)sk);
+            if (rc) return rc;
+            char* dst = out_pinned ? reinterpret_cast<char*>(X_out) + off : pout + off;
+            ODX_CUDA(cudaMemcpyAsync(dst, din + o_X + off, len, cudaMemcpyDeviceToHost, sk));
+            ODX_CUDA(cudaEventRecord(hc.ce[k], sk));
+            ODX_CUDA(cudaStreamWaitEvent(st, hc.ce[k], 0));
+        }
+        ODX_CUDA(cudaMemcpyAsync(pout + (o_out - o_X), din + o_out, out_bytes, cudaMemcpyDeviceToHost, st));
+        auto t4 = now();
+        ODX_CUDA(cudaStreamSynchronize(st));
+        auto t5 = now();
+        if (!out_pinned) CopyPool::get().copy(X_out, pout, nX);
+        if (timing) {
+            auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+            std::fprintf(stderr, "odx_solve_host (pipelined x%d) us: enqueue+pack %.1f sync %.1f unpack %.1f\n", K,
+                         us(t0, t4), us(t4, t5), us(t5, now()));
+        }
+    } else {
+
     if (!in_pinned) CopyPool::get().copy(pin + o_X, X_guess, nX);
     auto t1 = now();
     if (in_pinned) {
@@ -280,6 +352,12 @@ extern "C" int odx_solve_host(const odx_problem* P, const odx_stepper* S, const 
     auto t5 = now();
 
     if (!out_pinned) CopyPool::get().copy(X_out, pout, nX);
+    if (timing) {
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        std::fprintf(stderr, "odx_solve_host us: pack %.1f h2d-enq %.1f solve-enq %.1f d2h-enq %.1f sync %.1f unpack %.1f\n",
+                     us(t0, t1), us(t1, t2), us(t2, t3), us(t3, t4), us(t4, t5), us(t5, now()));
+    }
+    }
     const char* ob = pout + (o_out - o_X);
     std::memcpy(status_index, ob + o_sidx, (size_t)B * 8);
     std::memcpy(iters, ob + o_it, (size_t)B * 4);
@@ -295,11 +373,6 @@ extern "C" int odx_solve_host(const odx_problem* P, const odx_stepper* S, const 
             if (hist) hist[b * H + i] = (i <= last) ? hs[i] : qnan;
             if (scaled_hist) scaled_hist[b * H + i] = (i <= last) ? ss[i] : qnan;
         }
-    }
-    if (timing) {
-        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
-        std::fprintf(stderr, "odx_solve_host us: pack %.1f h2d-enq %.1f solve-enq %.1f d2h-enq %.1f sync %.1f unpack %.1f\n",
-                     us(t0, t1), us(t1, t2), us(t2, t3), us(t3, t4), us(t4, t5), us(t5, now()));
     }
     return ODX_OK;
 }
