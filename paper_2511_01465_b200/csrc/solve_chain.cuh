@@ -75,6 +75,22 @@ __device__ __forceinline__ void rows_issue(const double* X, const double* x0, lo
             return;
         }
     }
+    if constexpr (D == 2 && ITEMS % 2 == 1) {
+        if (r0 + ITEMS <= N) {
+            const double* src = X + r0 * 2;
+#pragma unroll
+            for (int q = 0; q < ITEMS; q++) ld_row2_nc(src + 2 * q, rw[2 + 2 * q], rw[3 + 2 * q]);
+            if (lane == 0) {
+                if (r0 == 0) {
+                    rw[0] = x0[0];
+                    rw[1] = x0[1];
+                } else {
+                    ld_row2_nc(src - 2, rw[0], rw[1]);
+                }
+            }
+            return;
+        }
+    }
     if constexpr (D == 1 && ITEMS % 2 == 0) {
         // d = 1: the thread's ITEMS rows as 16-byte pairs (r0 is even)
         if (r0 + ITEMS <= N) {
@@ -98,7 +114,7 @@ __device__ __forceinline__ void rows_issue(const double* X, const double* x0, lo
 template <int D, int ITEMS>
 __device__ __forceinline__ void rows_halo(long long N, long long r0, int lane,
                                           double (&rw)[(ITEMS + 1) * D]) {
-    if constexpr (D == 2 && ITEMS % 2 == 0) {
+    if constexpr (D == 2) {
         const double h0 = __shfl_up_sync(FULL, rw[2 * ITEMS], 1);
         const double h1 = __shfl_up_sync(FULL, rw[2 * ITEMS + 1], 1);
         if (lane > 0 && r0 + ITEMS <= N) {

@@ -47,8 +47,12 @@ namespace odx {
 // with four-warp groups); their 384-step tiles double the scanner's load, and a
 // cheap build (Euler, d = 1) or the small d = 3 tiles would run at the
 // scanner's rate (one hand-off per 32 tiles, ~0.19 us) — those keep four warps.
+#ifndef ODX_CHAIN2_WARPS
+#define ODX_CHAIN2_WARPS 8   // warps per CTA (experiment: 16 at 128 registers)
+#endif
 template <int D, int KIND, int S>
 constexpr int chain2_group_warps() {
+    if (ODX_CHAIN2_WARPS != 8) return 4;
     return (D == 2 && (KIND == 1 || S >= 3)) ? 2 : 4;
 }
 
@@ -56,15 +60,16 @@ template <int D, int NWV>
 struct Chain2Cfg {
     static constexpr int NW = NWV;      // warps per group (all compute)
     static constexpr int GT = NW * 32;  // threads per group
-    static constexpr int NG = 8 / NW;   // groups per CTA
+    static constexpr int NG = ODX_CHAIN2_WARPS / NW;   // groups per CTA
     static constexpr int NT = NG * GT;
     static constexpr int NWS = NG * NW;  // scanner warps (CTA 0)
-    static constexpr int ITEMS = D <= 2 ? 6 : 3;  // consecutive steps per thread
+    static constexpr int ITEMS = D <= 2 ? (ODX_CHAIN2_WARPS == 16 ? 3 : ODX_CHAIN2_WARPS == 12 ? 4 : 6)
+                                        : (ODX_CHAIN2_WARPS == 16 ? 1 : ODX_CHAIN2_WARPS == 12 ? 2 : 3);  // steps per thread
     static constexpr int T = GT * ITEMS;          // steps per tile
     static constexpr int LAG = 2;                 // tile i-LAG is applied in iteration i
     static constexpr int SL = LAG + 1;            // parked tiles
     static constexpr int E = D * D + D;
-    static constexpr int NP = D <= 2 ? 2 : 1;     // explicit steps built together
+    static constexpr int NP = (D <= 2 && ODX_CHAIN2_WARPS != 16) ? 2 : 1;  // explicit steps built together
     // scanner: tiles per lane — 64-tile windows for the 384-step tiles of two-warp
     // groups, i.e. one hand-off per 24576 steps either way (with 32-tile windows
     // the hand-off chain took 84% of cfg5's pass; a cheaper build would wait on it)
@@ -95,7 +100,7 @@ __device__ __forceinline__ long long rec_idx(long long t, int c) {
 }
 
 template <class P, int KIND, int S>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(ODX_CHAIN2_WARPS * 32, 1)
 chain2_pass_kernel(const ChainParams cp, const int it) {
     constexpr int D = P::D;
     using C = Chain2Cfg<D, chain2_group_warps<D, KIND, S>()>;
@@ -436,6 +441,9 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                     for (int q = 0; q < ITEMS / 2; q++)
                         ld256_nc(cur + r0 * 2 + 4 * q, xo[4 * q], xo[4 * q + 1], xo[4 * q + 2],
                                  xo[4 * q + 3]);
+                } else if (D == 2 && r0 + ITEMS <= N) {
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++) ld_row2_nc(cur + (r0 + q) * 2, xo[2 * q], xo[2 * q + 1]);
                 } else if (D == 1 && ITEMS % 2 == 0 && r0 + ITEMS <= N) {
 #pragma unroll
                     for (int q = 0; q < ITEMS / 2; q++)
