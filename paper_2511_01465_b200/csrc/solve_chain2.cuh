@@ -567,6 +567,34 @@ chain2_pass_kernel(const ChainParams cp, const int it) {
                 }
                 const long long r0 = ta * T + (long long)tid * ITEMS;
                 double xn[ITEMS * D];
+                if (zh && r0 + ITEMS <= N) {
+                    // full thread with an incoming state (every thread but the
+                    // trajectory's first): branch-free — all parked elements
+                    // loaded first, then the dependent chain; the row maxima
+                    // are reduced apart from it
+                    Elem<D> e[ITEMS];
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++) {
+#pragma unroll
+                        for (int c = 0; c < D * D; c++) e[q].F[c] = sm.els[g][s3][c][q * GT + tid];
+#pragma unroll
+                        for (int c = 0; c < D; c++) e[q].c[c] = sm.els[g][s3][D * D + c][q * GT + tid];
+                    }
+                    double rm[ITEMS];
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++) {
+                        double dx[D];
+                        apply<D>(e[q], z, dx);
+                        rm[q] = row_max_abs<D>(dx);
+#pragma unroll
+                        for (int k = 0; k < D; k++) {
+                            z[k] = dx[k];
+                            xn[q * D + k] = xo[q * D + k] + dx[k];
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < ITEMS; q++) step = nan_drop_max(step, rm[q]);
+                } else
 #pragma unroll
                 for (int q = 0; q < ITEMS; q++) {
                     if (r0 + q < N) {
