@@ -144,8 +144,11 @@ int odx_solve(const odx_problem* P, const odx_stepper* S,
  * solve() is called): x0 (B*d), X_guess (B*N*d) in; X_out (may alias
  * X_guess), hist / scaled_hist (B*(max_iters+1), entries past the iterations
  * run set to NaN; may be NULL), iters, status, status_index (B) out.  One H2D
- * and one D2H through cached pinned staging; blocks until the result is on the
- * host.  Device buffers and workspace are cached per device (grow-only). */
+ * and one D2H through cached pinned staging (a large batch of resident
+ * trajectories is cut into up to 8 batch chunks whose copies and solves
+ * overlap on internal streams, forked from and joined back into `stream`);
+ * blocks until the result is on the host.  Device buffers and workspace are
+ * cached per device (grow-only). */
 int odx_solve_host(const odx_problem* P, const odx_stepper* S,
                    const double* x0, const double* X_guess, double* X_out,
                    int64_t B, int64_t N, double dt, const odx_newton_cfg* C,
