@@ -219,6 +219,21 @@ struct SmallEngine {
                                                       const Elem<D> (&el)[ITEMS], Elem<D>& agg,
                                                       bool& has) {
         const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+        if (base + T <= N) {
+            // full tile (CTA-uniform): the same compositions in the same
+            // order without validity bits or branches
+            agg = el[0];
+#pragma unroll
+            for (int i = 1; i < ITEMS; i++) compose<D>(agg, el[i], agg);
+            has = true;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                Elem<D> o, t;
+                shfl_up_elem<D>(agg, o, off);
+                compose<D>(o, agg, t);
+                if (lane >= off) agg = t;
+            }
+        } else {
         has = false;
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
@@ -234,6 +249,7 @@ struct SmallEngine {
         }
         if (!has) set_identity<D>(agg);
         warp_inclusive_scan<D>(agg, has, lane);
+        }
         if (lane == 31) {
 #pragma unroll
             for (int i = 0; i < D * D; i++) sm.wtF[w][i] = agg.F[i];
@@ -290,6 +306,26 @@ struct SmallEngine {
         shfl_up_elem<D>(agg, ex, 1);
         bool exh = __shfl_up_sync(FULL, has, 1) && lane > 0;
         if (exh) apply<D>(ex, z, z);
+        if (base + (long long)(tid + 1) * ITEMS <= N) {
+            // full thread: the same operations in the same order, branch-free;
+            // the row maxima are reduced apart from the dependent chain
+            double rm[ITEMS];
+#pragma unroll
+            for (int i = 0; i < ITEMS; i++) {
+                const int r = tid * ITEMS + i;
+                double dx[D];
+                apply<D>(el[i], z, dx);
+                rm[i] = row_max_abs<D>(dx);
+#pragma unroll
+                for (int j = 0; j < D; j++) {
+                    z[j] = dx[j];
+                    sm.xs[L::idx((r + 1) * D + j)] += dx[j];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < ITEMS; i++) step = nan_drop_max(step, rm[i]);
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < ITEMS; i++) {
             const int r = tid * ITEMS + i;
@@ -320,9 +356,6 @@ resident_solve_kernel(const SolveParams p) {
     using L = typename E::L;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typename E::Shared& sm = *reinterpret_cast<typename E::Shared*>(smem_raw);
-    __shared__ double dec_rn, dec_sc;
-    __shared__ unsigned long long dec_bad;
-
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const long long b = blockIdx.x;
     const long long N = p.N;
@@ -334,6 +367,7 @@ resident_solve_kernel(const SolveParams p) {
         long long row = i / D - 1;
         sm.xs[L::idx(i)] = (row < 0) ? p.x0[b * D + i] : Xb[i - D];
     }
+    if (tid < D) sm.z[tid] = 0.0;  // the trajectory starts in this tile: no incoming offset
     __syncthreads();
 
     double step_prev = __longlong_as_double(0x7ff8000000000000ll);  // NaN
@@ -358,43 +392,39 @@ resident_solve_kernel(const SolveParams p) {
         scn = warp_max_nan_drop(scn);
         bad = warp_min_u64(bad);
         if (lane == 0) { sm.redd[0][w] = rn; sm.redd[1][w] = scn; sm.redb[w] = bad; }
-        __syncthreads();
-        if (tid == 0) {
-            double a = 0.0, c = 0.0;
-            unsigned long long m = ~0ull;
-            for (int q = 0; q < NW; q++) {
-                a = fmax(a, sm.redd[0][q]);
-                c = fmax(c, sm.redd[1][q]);
-                m = sm.redb[q] < m ? sm.redb[q] : m;
-            }
-            dec_rn = a; dec_sc = (KIND == 0) ? a : c; dec_bad = m;
-        }
-        __syncthreads();
-        const double rnb = dec_rn;
-        dd = decide(it, p, rnb, dec_bad, step_prev);
-        if (tid == 0 && dd.status != ODX_ST_SINGULAR) {
-            if (p.hist) p.hist[b * H + it] = rnb;
-            if (p.shist) p.shist[b * H + it] = dec_sc;
-        }
-        if (dd.stop) break;
-
+        // The block scan does not depend on the decision (and changes no
+        // state), so it runs before the iteration's first barrier; every
+        // thread then reduces the warps' residuals itself (same order as a
+        // single thread would) — two barriers per iteration instead of five.
         Elem<D> agg;
         bool has;
         E::block_scan(sm, 0, N, el, agg, has);
-        if (tid == 0) {
-#pragma unroll
-            for (int r = 0; r < D; r++) sm.z[r] = 0.0;
-        }
         __syncthreads();
+        double rnb = 0.0, scb = 0.0;
+        unsigned long long badb = ~0ull;
+#pragma unroll
+        for (int q = 0; q < NW; q++) {
+            rnb = fmax(rnb, sm.redd[0][q]);
+            scb = fmax(scb, sm.redd[1][q]);
+            badb = sm.redb[q] < badb ? sm.redb[q] : badb;
+        }
+        if (KIND == 0) scb = rnb;
+        dd = decide(it, p, rnb, badb, step_prev);
+        if (tid == 0 && dd.status != ODX_ST_SINGULAR) {
+            if (p.hist) p.hist[b * H + it] = rnb;
+            if (p.shist) p.shist[b * H + it] = scb;
+        }
+        if (dd.stop) break;
+
         double step = 0.0;
         E::apply_items(sm, 0, N, el, agg, has, step);
         step = warp_max_nan_drop(step);
         if (lane == 0) sm.redd[2][w] = step;
         __syncthreads();
         double s = 0.0;
+#pragma unroll
         for (int q = 0; q < NW; q++) s = fmax(s, sm.redd[2][q]);
         step_prev = s;
-        __syncthreads();
     }
     for (int i = tid; i < (int)(N * D); i += THREADS) Xb[i] = sm.xs[L::idx(i + D)];
     if (tid == 0) {
