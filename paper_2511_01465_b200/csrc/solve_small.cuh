@@ -290,7 +290,21 @@ struct SmallEngine {
         double z[D];
 #pragma unroll
         for (int r = 0; r < D; r++) z[r] = sm.z[r];
-        // warp-exclusive: warp totals 0..w-1 applied in order
+        // warp-exclusive: warp totals 0..w-1 applied in order (full tiles:
+        // unrolled, so the next total's loads overlap the current apply)
+        if (base + T <= N) {
+#pragma unroll
+            for (int q = 0; q < NW - 1; q++) {
+                if (q < w) {
+                    Elem<D> e;
+#pragma unroll
+                    for (int i = 0; i < D * D; i++) e.F[i] = sm.wtF[q][i];
+#pragma unroll
+                    for (int i = 0; i < D; i++) e.c[i] = sm.wtc[q][i];
+                    apply<D>(e, z, z);
+                }
+            }
+        } else
 #pragma unroll 1
         for (int q = 0; q < w; q++) {
             if (!sm.wthas[q]) continue;
