@@ -8,6 +8,7 @@ arithmetic differences from the reference).
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -18,6 +19,12 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-9
+# Residual histories, scaled by the largest entry like the states.  Observed on
+# B200 (ODX_TEST_RECORD run, profiles/r2/parity_margins_r2h.txt): <= 2.8e-10 on
+# every case but the 300k-step stiff trajectories of
+# test_persistent_large_vs_oracle (2.3e-8: the residual of an amplified iterate).
+HIST_TOL = 1e-9
+HIST_TOL_LONG = 1e-7
 
 
 def scaled_close(x, ref, tol=TOL, what=""):
@@ -35,6 +42,12 @@ def scaled_close(x, ref, tol=TOL, what=""):
         return 0.0
     scale = max(1.0, float(np.max(np.abs(ref[fin_ref]))))
     err = float(np.max(np.abs(x[fin_ref] - ref[fin_ref])))
+    if os.environ.get("ODX_TEST_RECORD"):  # diagnostic: observed margins, one line per check
+        with open(os.environ["ODX_TEST_RECORD"], "a") as fh:
+            rel = np.abs(x[fin_ref] - ref[fin_ref]) / np.maximum(np.abs(ref[fin_ref]), 1e-300)
+            fh.write(f"{os.environ.get('PYTEST_CURRENT_TEST', '?')} | {what} | tol {tol:.0e} | "
+                     f"scaled {err / scale:.3e} | max rel {float(rel.max()):.3e} | "
+                     f"min |ref| {float(np.abs(ref[fin_ref]).min()):.3e} | n {int(fin_ref.sum())}\n")
     assert err <= tol * scale, f"{what}: max err {err:.3e} > {tol:.1e} * {scale:.3e}"
     return err / scale
 
@@ -171,7 +184,7 @@ def test_solve_reference_problems(pkg, oracle, golden_solves, case):
     rep = pkg.solve(prob, st, dt, policy, pkg.NewtonConfig(max_iters=iters))
     ref = _oracle_ref_solve(oracle, name, sname, dt, policy, iters)
     assert rep.iterations_run == ref["iters"] == iters
-    scaled_close(np.array(rep.residual_history), ref["hist"], 1e-7, "hist")
+    scaled_close(np.array(rep.residual_history), ref["hist"], HIST_TOL, "hist")
     scaled_close(rep.trajectory.states, ref["X"], TOL, "states")
 
 
@@ -335,7 +348,7 @@ def test_persistent_large_vs_oracle(pkg, oracle, case):
     ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), x0, np.tile(x0, (n, 1)), dt,
                        iters, abort_nonfinite=False)
     assert int(r.iterations_run[0]) == ref["iters"]
-    scaled_close(r.residual_history[0], ref["hist"], 1e-7, "hist")
+    scaled_close(r.residual_history[0], ref["hist"], HIST_TOL_LONG, "hist")
     # Robertson (k2 = 3e7) is stiff: rounding differences are amplified by the
     # conditioning of the 200k-step recursion, so use the reference's own
     # implicit-path tolerance (test_acceptance.py crit 5: 1e-8)
@@ -391,7 +404,7 @@ def test_cfg4_small_vs_golden(pkg, golden_baseline):
     r1 = _gpu_cfg_solve(pkg, cfg, n=512, max_iters=1, step_tol=0.0, abort=False)
     scaled_close(r1.states[0], g["cfg4t_X1"], TOL, "N=512 iterate 1")
     r3 = _gpu_cfg_solve(pkg, cfg, n=512, max_iters=3, step_tol=0.0, abort=False)
-    scaled_close(r3.residual_history[0], g["cfg4t_hist"], 1e-7, "N=512 hist")
+    scaled_close(r3.residual_history[0], g["cfg4t_hist"], HIST_TOL, "N=512 hist")
     scaled_close(r3.states[0], g["cfg4t_X"], TOL, "N=512 iterate 3")
 
 
@@ -415,7 +428,7 @@ def test_cfg4_full_size_first_iterates(pkg, oracle):
     ref = oracle.solve(7, cfg.params, oracle.stepper_by_name("backward_euler"), x0,
                        np.tile(x0, (cfg.n_steps, 1)), cfg.dt, 1, abort_nonfinite=False)
     r1 = _gpu_cfg_solve(pkg, cfg, max_iters=1, step_tol=0.0, abort=False)
-    scaled_close(r1.residual_history[0][:2], ref["hist"], 1e-7, "hist")
+    scaled_close(r1.residual_history[0][:2], ref["hist"], HIST_TOL, "hist")
     scaled_close(r1.states[0], ref["X"], TOL, "full-N iterate 1")
     r = _gpu_cfg_solve(pkg, cfg)
     assert int(r.status[0]) == 0 and int(r.iterations_run[0]) == 100  # MAXITER
@@ -489,7 +502,7 @@ def test_path_boundaries_vs_oracle(pkg, oracle, n, sname):
     ref = oracle.solve(1, (mu,), oracle.stepper_by_name(sname), x0, np.tile(x0, (n, 1)), dt, 3,
                        abort_nonfinite=False)
     assert int(r.iterations_run[0]) == ref["iters"] and int(r.status[0]) == ref["status"]
-    scaled_close(r.residual_history[0], ref["hist"], 1e-7, f"N={n} hist")
+    scaled_close(r.residual_history[0], ref["hist"], HIST_TOL, f"N={n} hist")
     scaled_close(r.states[0], ref["X"], TOL, f"N={n} states")
 
 
@@ -552,7 +565,7 @@ def test_grid_resident_stress_cold_memory(pkg, oracle):
     for _ in range(4):
         sweep.fill_(0.0)
         r = solve_batch(prob, st, dt, x0[None], None, conf)
-        scaled_close(r.residual_history[0], ref["hist"], 1e-7, "hist")
+        scaled_close(r.residual_history[0], ref["hist"], HIST_TOL, "hist")
         scaled_close(r.states[0], ref["X"], TOL, "states")
     del sweep
 
@@ -590,7 +603,7 @@ def test_solve_with_device_built_guess(pkg, oracle):
     ref = oracle.solve(1, (1.0,), oracle.stepper_by_name("rk4"), np.array([2.0, 0.0]), g, dt, 3,
                        abort_nonfinite=True)
     assert rep.iterations_run == ref["iters"]
-    scaled_close(np.asarray(rep.residual_history), ref["hist"], 1e-7, "hist")
+    scaled_close(np.asarray(rep.residual_history), ref["hist"], HIST_TOL, "hist")
     scaled_close(np.asarray(rep.trajectory.states), ref["X"], 1e-9, "states")
 
 
@@ -764,7 +777,7 @@ def test_batched_long_trajectories(pkg, oracle, case):
         ref = oracle.solve(pid, params, oracle.stepper_by_name(sname), x0s[b],
                            np.tile(x0s[b], (n, 1)), dt, 3, abort_nonfinite=False)
         assert int(r.iterations_run[b]) == ref["iters"] and int(r.status[b]) == ref["status"]
-        scaled_close(r.residual_history[b], ref["hist"], 1e-7, f"b={b} hist")
+        scaled_close(r.residual_history[b], ref["hist"], HIST_TOL, f"b={b} hist")
         scaled_close(r.states[b], ref["X"], TOL, f"b={b} states")
 
 
