@@ -379,12 +379,14 @@ def e2e_steps(w: Workload, steps: int, warmup: int):
 
 
 def sharded_e2e(tw, steps: int, warmup: int, world: int):
-    """Time-sharded e2e: each rank copies its chunk of the host guess in, runs
-    its part of the solve and copies its chunk of the trajectory out; max over
-    ranks of the event-timed step."""
+    """Time-sharded e2e, defined like the N = 1 line's: each rank builds its
+    chunk of the replicate_x0 guess on the device from x0 (d * 8 bytes in),
+    runs its part of the solve and copies its chunk of the trajectory out to
+    pinned host memory; max over ranks of the event-timed step."""
     torch = tw.torch
+    from paper_2511_01465_b200.newton_pint import initial_guess_device
     from paper_2511_01465_b200.sharded import solve_time_sharded
-    host_guess = tw.guess.cpu().numpy()
+    out = torch.empty(tuple(tw.X.shape), dtype=torch.float64, pin_memory=True)
     durs = []
     for k in range(warmup + steps):
         e0 = torch.cuda.Event(enable_timing=True)
@@ -392,17 +394,16 @@ def sharded_e2e(tw, steps: int, warmup: int, world: int):
         torch.distributed.barrier()
         torch.cuda.synchronize()
         e0.record()
-        tw.X.copy_(torch.from_numpy(host_guess), non_blocking=False)
-        solve_time_sharded(tw.prob, tw.stepper, tw.cfg.dt, tw.X, tw.off, tw.conf)
-        out = tw.X.cpu()
+        X = initial_guess_device("replicate_x0", tw.prob, tw.n)[0]
+        solve_time_sharded(tw.prob, tw.stepper, tw.cfg.dt, X, tw.off, tw.conf)
+        out.copy_(X, non_blocking=True)
         e1.record()
         torch.cuda.synchronize()
         if k >= warmup:
             durs.append(e0.elapsed_time(e1))
-        del out
+        del X
     tot = reduce_max(sum(durs), world)
-    nb = host_guess.nbytes
-    return tot / len(durs), nb, nb
+    return tot / len(durs), tw.d * 8, out.numel() * 8
 
 
 def reduce_max(v: float, world: int) -> float:
@@ -543,12 +544,21 @@ def main():
         return
     import torch
     torch.cuda.set_device(local)
-    if world > 1:
+    # ODX_BENCH_FORCE_SHARDED=1 (diagnostic): take the N > 1 branches at world
+    # size 1 through a real NCCL group, so the scaling run's code path can be
+    # exercised on a one-GPU box (tools/check_bench_sharded.py)
+    multi = world > 1 or os.environ.get("ODX_BENCH_FORCE_SHARDED") == "1"
+    if multi:
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm, hbm_src, fp64, fp64_src = peaks()
     cid = cfg_id(args.workload)
-    if cid == 5 and world > 1:
+    if cid == 5 and multi:
         w = TimeShardedWorkload(cid, args.iters, rank, world)
     else:
         w = Workload(cid, args.iters, rank=rank, world=world)
@@ -558,7 +568,7 @@ def main():
         flush_l2(flush_buf)
 
     clocks = Clocks(local)
-    if world > 1:
+    if multi:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -579,7 +589,8 @@ def main():
         # result chunk device->host (max over ranks)
         e2e_ms, h2d, d2h = sharded_e2e(w, max(3, args.steps // 2), 1, world)
         e2e_val = units_per_step / (e2e_ms * 1e-3)
-        guess_note = "host numpy guess chunk per rank copied in; result chunk copied out"
+        guess_note = ("replicate_x0 chunk built on the device per rank (odx_initial_guess) from "
+                      "x0; result chunk copied out to pinned host memory")
     else:
         # e2e through the public API with host buffers
         e2e_durs, h2d, d2h, guess_note = e2e_steps(w, max(5, args.steps // 2),
@@ -617,7 +628,7 @@ def main():
             pass
 
     extra = {}
-    if not args.no_extra and world == 1:
+    if not args.no_extra and not multi:
         for ocid in (o for o in (1, 2, 3, 4, 5) if o != cid):
             try:
                 ow = Workload(ocid, args.iters)
@@ -658,7 +669,7 @@ def main():
             except Exception as exc:  # report, never hide
                 extra[f"cfg{ocid}"] = {"error": f"{type(exc).__name__}: {exc}"}
 
-    if not args.no_extra and world > 1:
+    if not args.no_extra and multi:
         # cfg5's and cfg4's one trajectory split along time over the N ranks
         # (one NCCL all-gather per iteration): strong scaling against the N = 1
         # run's configs["cfg5_..."] / ["cfg4_..."] entries (same flush, same
@@ -724,7 +735,7 @@ def main():
             "configs": extra,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
 

@@ -1,5 +1,10 @@
 """Exercise bench.py's N > 1 time-sharded cfg5 entry at world size 1 (the
-code path the driver's scaling run takes, with a real NCCL process group)."""
+code path the driver's scaling run takes, with a real NCCL process group).
+
+The whole main() of the N > 1 run (headline line, sharded e2e, the
+configs["cfg4_time_sharded"] entry) can be exercised the same way:
+    ODX_BENCH_FORCE_SHARDED=1 python bench.py --steps 5 --warmup 3 --no-cpu
+(profiles/r2/bench_forced_sharded_w1_r2h.json)."""
 import os
 import socket
 import sys
