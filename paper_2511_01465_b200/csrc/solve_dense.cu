@@ -218,7 +218,10 @@ dense_lu_build_kernel(const DenseParams p, int it) {
 // K1 fast path: periodic-tridiagonal band LU, one warp per step (dense_band.cuh)
 // =========================================================================
 template <class DP>
-__global__ void __launch_bounds__(BAND_WARPS * 32, 3)
+#ifndef ODX_BAND_MINB
+#define ODX_BAND_MINB 3  // CTAs per SM the register budget is set for (168 registers)
+#endif
+__global__ void __launch_bounds__(BAND_WARPS * 32, ODX_BAND_MINB)
 dense_band_build_kernel(const DenseParams p, int it) {
     if (p.st && p.st->stopped) return;
     __shared__ BandWarpSmem bsm[BAND_WARPS];
